@@ -1,0 +1,181 @@
+/*
+ * ctis.h — C ABI of libctis: the B200 (sm_100a) hot path of the shift-invariant
+ * CTIS MLEM reconstruction of arXiv 2006.01573 (White, Bell, Haygood).
+ *
+ * The operator (PAPER.md line numbers, "P:<line>"):
+ *   A CTIS maps a datacube f (a x alpha field stop, w wavelength bands) onto an
+ *   FPA image g (gamma x xi pixels) by the linear model g = H f (Eq. 1).
+ *   By shift-invariance H = (C_1 E ... C_w E) (Eqs. 3-8): E embeds a
+ *   band's a x alpha block into the FPA (Eqs. 5-6; index map P:131-133)
+ *   and C_lambda is the n x n circulant whose first column c_lambda is the band's
+ *   calibration image for a point source at field-stop pixel (0,0) (Eq. 7;
+ *   P:24).  This library stores each c_lambda as a sparse list of taps
+ *   (offset o, weight w): o is the column-major FPA index of a nonzero of
+ *   c_lambda, so voxel (r, c) of band lambda adds w * f to FPA pixel
+ *   (r + gamma*c + o) mod n — exactly the 1-D circulant of Eq. 7, including the
+ *   carry into the next FPA column and the wrap past pixel n-1.
+ *
+ * Layouts (column-major everywhere, reading R1; P:24 allows either):
+ *   f      float32[w][alpha][a]   element (lam, c, r) at lam*a*alpha + c*a + r    (Eq. 9)
+ *   g, g_hat, r  float32[xi][gamma]  pixel (R, C) at R + gamma*C
+ *   batched:  g[F][n], f[F][m] (frame-major, contiguous).
+ *
+ * Conventions for every entry point:
+ *   - sizes are int64_t; n = gamma*xi, l = a*alpha, m = l*w (or l*(band_end-band_begin)
+ *     for a shard plan, "m_local"); n and m must be < 2^31.
+ *   - float* arguments of the stream-ordered calls are DEVICE pointers on the plan's
+ *     device, owned by the caller, 16-byte aligned, non-overlapping unless stated.
+ *     The plan owns only its tap tables and a few bytes of scratch.
+ *   - calls are stream-ordered and asynchronous: CTIS_OK means "validated and
+ *     enqueued on `stream`" (NULL = the legacy default stream).  Kernel faults
+ *     surface as CTIS_ERR_CUDA on a later call or at stream synchronisation.
+ *   - on any error nothing is enqueued, outputs are unspecified, inputs untouched;
+ *     ctis_last_error() gives a one-line reason (thread-local).
+ *   - a plan may be used from several host threads, calls are serialised internally.
+ *   - no CPU fallback: every arithmetic step runs in sm_100a kernels; on a device
+ *     that is not compute capability 10.x plan creation fails with CTIS_ERR_UNSUPPORTED.
+ */
+#ifndef CTIS_H_
+#define CTIS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define CTIS_API __attribute__((visibility("default")))
+#else
+#define CTIS_API
+#endif
+
+typedef struct ctis_plan_s* ctis_plan;
+/* Identical to cudaStream_t (struct CUstream_st*). */
+typedef struct CUstream_st* ctis_stream;
+
+typedef enum {
+  CTIS_OK = 0,
+  CTIS_ERR_INVALID_ARGUMENT = 1, /* null pointer, iters < 0, frames < 1, misaligned pointer,
+                                    wrong call for the plan kind (mlem on a shard plan) */
+  CTIS_ERR_DIMENSION = 2,        /* a, alpha, w, gamma, xi < 1; gamma < a; xi < alpha; n or m >= 2^31;
+                                    band range outside [0, w) or empty */
+  CTIS_ERR_TAP = 3,              /* tap_ptr not a CSR over w bands; offset outside [0, n);
+                                    weight <= 0 or non-finite; duplicate offset within a band;
+                                    band with no taps */
+  CTIS_ERR_ZERO_SENSITIVITY = 4, /* h_lambda = sum_t w_t not > 0 in float32 */
+  CTIS_ERR_DATA = 5,             /* g or f0 negative, NaN or Inf (validated by ctis_mlem*) */
+  CTIS_ERR_CUDA = 6,             /* CUDA runtime error; see ctis_last_error() */
+  CTIS_ERR_OUT_OF_MEMORY = 7,
+  CTIS_ERR_UNSUPPORTED = 8       /* device is not compute capability 10.x (sm_100) */
+} ctis_status;
+
+/* Options for ctis_set_option. */
+typedef enum {
+  CTIS_OPT_VALIDATE_DATA = 1,   /* 1 (default): ctis_mlem* check g >= 0, f0 >= 0, finite, with one
+                                   reduction kernel and ONE host synchronisation per call;
+                                   0: skip (the call is then fully asynchronous). */
+  CTIS_OPT_USE_GRAPH = 2        /* 1 (default): ctis_mlem* replay a captured CUDA graph of the
+                                   iterations; 0: launch kernels directly on `stream`. */
+} ctis_option;
+
+/* Create a plan for the full operator H (all w bands).
+ *   a, alpha   field stop rows x columns
+ *   w          number of wavelength bands
+ *   gamma, xi  FPA rows x columns
+ *   tap_ptr    HOST, w+1 entries, CSR: band lam owns taps [tap_ptr[lam], tap_ptr[lam+1])
+ *   tap_offset HOST, column-major FPA index in [0, n) of a nonzero of c_lam
+ *   tap_weight HOST, the value of c_lam there: finite, > 0
+ *   device     CUDA device ordinal the plan (and every buffer passed to it) lives on
+ * The calibration is copied and pre-processed (sorted, split into rectangle
+ * pieces, binned per FPA tile); the host arrays may be freed on return.
+ * The per-band sensitivity h_lam = sum_t w_t (every column of a circulant
+ * block has the same sum) is computed in double and must be > 0. */
+CTIS_API ctis_status ctis_plan_create(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi,
+                             const int64_t* tap_ptr, const int64_t* tap_offset,
+                             const float* tap_weight, int device, ctis_plan* out);
+
+/* Latency-mode shard plan: same full CSR, but the plan keeps only bands
+ * [band_begin, band_end) (Eq. 3: H's block columns).  Its f is the
+ * m_local = a*alpha*(band_end-band_begin) slice of those bands; ctis_forward
+ * writes the PARTIAL sum over its bands (summed across shards by the caller's
+ * collective); ctis_mlem / ctis_mlem_batched return CTIS_ERR_INVALID_ARGUMENT. */
+CTIS_API ctis_status ctis_plan_create_shard(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi,
+                                   const int64_t* tap_ptr, const int64_t* tap_offset,
+                                   const float* tap_weight, int64_t band_begin, int64_t band_end,
+                                   int device, ctis_plan* out);
+
+CTIS_API void ctis_plan_destroy(ctis_plan plan);
+
+/* Plan dimensions: out[0..9] = a, alpha, w_local, gamma, xi, n, m_local, band_begin,
+ * band_end, total taps stored.  Host-side, no device work. */
+CTIS_API ctis_status ctis_plan_dims(ctis_plan plan, int64_t out[10]);
+
+CTIS_API ctis_status ctis_set_option(ctis_plan plan, int option, int64_t value);
+
+/* Bytes of caller-allocated device workspace needed by ctis_mlem* and
+ * ctis_back_update_from_ghat for `frames` frames (frames >= 1): holds r = g / g_hat. */
+CTIS_API size_t ctis_workspace_bytes(ctis_plan plan, int64_t frames);
+
+/* g_hat = H f (Eqs. 8-13): f[m_local] -> g_hat[n], overwritten. */
+CTIS_API ctis_status ctis_forward(ctis_plan plan, const float* f, float* g_hat, ctis_stream stream);
+
+/* Batched forward: f[frames][m_local] -> g_hat[frames][n]. */
+CTIS_API ctis_status ctis_forward_batched(ctis_plan plan, const float* f, float* g_hat, int64_t frames,
+                                 ctis_stream stream);
+
+/* z = H^T r (Eqs. 14-17): r[n] -> z[m_local], overwritten. */
+CTIS_API ctis_status ctis_backproject(ctis_plan plan, const float* r, float* z, ctis_stream stream);
+
+/* h = H^T 1: h[m_local], overwritten; h_j = sum of band lam(j)'s tap weights. */
+CTIS_API ctis_status ctis_sensitivity(ctis_plan plan, float* h, ctis_stream stream);
+
+/* MLEM (Eq. 2, Alg. 1): `iters` iterations of
+ *   g_hat = H f;  r = g (/) g_hat  (r_p = 0 where g_hat_p = 0);  f <- f (.) (H^T r) (/) h
+ * in place on f (in: f^(1), out: f^(iters+1)); g[n] is read only; ws must hold
+ * ctis_workspace_bytes(plan, 1) bytes.  iters = 0 leaves f unchanged. */
+CTIS_API ctis_status ctis_mlem(ctis_plan plan, const float* g, float* f, int iters, void* ws,
+                      ctis_stream stream);
+
+/* Snapshot-video batch: `frames` independent reconstructions sharing the plan;
+ * g[frames][n], f[frames][m] in place, ws >= ctis_workspace_bytes(plan, frames). */
+CTIS_API ctis_status ctis_mlem_batched(ctis_plan plan, const float* g, float* f, int64_t frames, int iters,
+                              void* ws, ctis_stream stream);
+
+/* The two fused kernels of one MLEM iteration, exposed for step-wise drivers and timing:
+ *   ctis_forward_ratio: r = g (/) (H f), r_p = 0 where (H f)_p = 0     (Alg. 1 lines 6-8)
+ *                       f[m], g[n] -> r[n] (r may be the ctis_mlem workspace)
+ *   ctis_back_update:   f <- f (.) (H^T r) (/) h, in place             (Alg. 1 lines 9-12) */
+CTIS_API ctis_status ctis_forward_ratio(ctis_plan plan, const float* f, const float* g, float* r,
+                                        ctis_stream stream);
+CTIS_API ctis_status ctis_back_update(ctis_plan plan, const float* r, float* f, ctis_stream stream);
+
+/* Latency mode, second half of an iteration on a shard plan: given the measured
+ * g[n] and the all-reduced g_hat[n] = H f (sum over all shards), compute
+ * r = g (/) g_hat into ws and update this shard's f[m_local] <- f (.) (H_shard^T r) (/) h. */
+CTIS_API ctis_status ctis_back_update_from_ghat(ctis_plan plan, const float* g, const float* g_hat, float* f,
+                                       void* ws, ctis_stream stream);
+
+/* End-to-end convenience on HOST buffers: copies g_host[frames][n] and
+ * f_host[frames][m] (f0) to plan-owned device buffers, runs ctis_mlem_batched,
+ * copies f back into f_host and synchronises `stream` before returning.
+ * Pinned host memory gives full PCIe/NVLink-C2C bandwidth; pageable works too. */
+CTIS_API ctis_status ctis_mlem_host(ctis_plan plan, const float* g_host, float* f_host, int64_t frames,
+                           int iters, ctis_stream stream);
+
+/* Number of kernel launches the last ctis_* call on this plan enqueued (graph
+ * replays count the kernels inside the graph). */
+CTIS_API int64_t ctis_last_launch_count(ctis_plan plan);
+
+/* One-line description of the last error on this host thread ("" if none). */
+CTIS_API const char* ctis_last_error(void);
+
+/* Library version string. */
+CTIS_API const char* ctis_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CTIS_H_ */

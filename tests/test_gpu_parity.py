@@ -1,0 +1,279 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle.
+
+Tolerances (BASELINE.json north_star): relative L2 <= 1e-5 for one forward or
+back projection, <= 1e-3 on f after the configuration's MLEM iterations.
+A single unit tap at offset 0 must be bit-exact (H is then a 0/1 selection).
+"""
+import numpy as np
+import pytest
+
+import ctis_synth as syn
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+PROJ_TOL = 1e-5
+MLEM_TOL = 1e-3
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64).reshape(-1)
+    b = np.asarray(b, np.float64).reshape(-1)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def ctis():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2006_01573_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return torch.device("cuda:0")
+
+
+def cuda(x, dev):
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, np.float32).reshape(-1))).to(dev)
+
+
+# ------------------------------------------------------------------ single projections at every config size
+@pytest.mark.parametrize("name", ["tiny", "C2", "C3", "C4"])
+def test_forward_back_paper_configs(ctis, oracle_lib, dev, name):
+    cfg = syn.config(name)
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    f = syn.scene_blobs(geom)
+    gh = plan.forward(cuda(f, dev))
+    want = oracle_lib.forward(geom, taps, f)
+    assert rel(gh.cpu().numpy(), want) <= PROJ_TOL
+    u = np.random.default_rng(1).uniform(0.5, 1.5, geom.n).astype(np.float32)
+    z = plan.backproject(cuda(u, dev))
+    assert rel(z.cpu().numpy(), oracle_lib.backproject(geom, taps, u)) <= PROJ_TOL
+    h = plan.sensitivity()
+    assert rel(h.cpu().numpy(), oracle_lib.sensitivity(geom, taps)) <= 1e-6
+
+
+GEOMS = [
+    syn.Geometry(1, 1, 1, 1, 1),            # degenerate: n = 1
+    syn.Geometry(3, 5, 2, 3, 5),            # field stop fills the FPA
+    syn.Geometry(7, 5, 3, 40, 29),          # ragged everything
+    syn.Geometry(33, 17, 6, 70, 45),        # several tiles + ragged tails
+    syn.Geometry(65, 40, 9, 130, 100),      # > 2 forward tiles in both directions
+    syn.Geometry(128, 32, 5, 200, 33),
+]
+
+
+@pytest.mark.parametrize("gi", range(len(GEOMS)))
+@pytest.mark.parametrize("region", ["any", "nowrap"])
+def test_forward_back_random_wrapping_taps(ctis, oracle_lib, dev, gi, region):
+    geom = GEOMS[gi]
+    taps = syn.random_taps(geom, (1, 13), seed=10 + gi, region=region)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    rng = np.random.default_rng(gi)
+    f = rng.random(geom.m).astype(np.float32)
+    u = rng.random(geom.n).astype(np.float32)
+    assert rel(plan.forward(cuda(f, dev)).cpu().numpy(), oracle_lib.forward(geom, taps, f)) <= PROJ_TOL
+    assert rel(plan.backproject(cuda(u, dev)).cpu().numpy(), oracle_lib.backproject(geom, taps, u)) <= PROJ_TOL
+
+
+def test_unit_tap_is_bit_exact_embed_extract(ctis, oracle_lib, dev):
+    geom = syn.Geometry(37, 21, 3, 100, 50)
+    taps = syn.Taps(np.array([0, 1, 2, 3]), np.array([0, 0, 0]), np.ones(3, np.float32))
+    plan = ctis.Plan.from_geometry(geom, taps)
+    f = np.random.default_rng(3).random(geom.m).astype(np.float32)
+    got = plan.forward(cuda(f, dev)).cpu().numpy()
+    assert np.array_equal(got, oracle_lib.forward(geom, taps, f).astype(np.float32))
+    u = np.random.default_rng(4).random(geom.n).astype(np.float32)
+    z = plan.backproject(cuda(u, dev)).cpu().numpy()
+    assert np.array_equal(z, oracle_lib.backproject(geom, taps, u).astype(np.float32))
+
+
+def test_full_wrap_taps_bit_exact_single_tap_per_band(ctis, oracle_lib, dev):
+    """One tap per band at offsets that carry and wrap: still a permutation -> bit-exact."""
+    geom = syn.Geometry(9, 6, 3, 20, 11)
+    n = geom.n
+    offs = np.array([n - 1, geom.gamma - 2, n - geom.gamma * 3 + 5])
+    taps = syn.Taps(np.array([0, 1, 2, 3]), offs, np.ones(3, np.float32))
+    plan = ctis.Plan.from_geometry(geom, taps)
+    f = np.random.default_rng(5).random(geom.m).astype(np.float32)
+    assert np.array_equal(plan.forward(cuda(f, dev)).cpu().numpy(),
+                          oracle_lib.forward(geom, taps, f).astype(np.float32))
+
+
+# ------------------------------------------------------------------ MLEM
+def _mlem_case(ctis, oracle_lib, dev, geom, taps, K, ftrue):
+    g = oracle_lib.forward(geom, taps, ftrue).astype(np.float32)
+    want = oracle_lib.mlem(geom, taps, g, np.ones(geom.m), K)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    gd = cuda(g, dev)
+    fd = torch.ones(geom.m, dtype=torch.float32, device=dev)
+    plan.mlem(gd, fd, K)
+    return rel(fd.cpu().numpy(), want), plan, gd, fd
+
+
+@pytest.mark.parametrize("name", ["tiny", "C2", "C3"])
+def test_mlem_paper_configs(ctis, oracle_lib, dev, name):
+    cfg = syn.config(name)
+    r, *_ = _mlem_case(ctis, oracle_lib, dev, cfg.geom, syn.paper_taps(cfg), cfg.K, syn.scene_blobs(cfg.geom))
+    assert r <= MLEM_TOL, r
+
+
+def test_mlem_C4_first_iterations_vs_oracle(ctis, oracle_lib, dev):
+    """Full C4 size: 2 iterations against the oracle (the oracle needs ~5 s per iteration)."""
+    cfg = syn.config("C4")
+    r, *_ = _mlem_case(ctis, oracle_lib, dev, cfg.geom, syn.paper_taps(cfg), 2, syn.scene_blobs(cfg.geom))
+    assert r <= 1e-5, r
+
+
+def test_mlem_C4_full_run_invariants(ctis, dev):
+    """Full C4 run (K=100) in the bench's launch configuration: properties that hold at any size —
+    nonnegativity and count conservation sum(H f^(k+1)) = sum_{ghat^(k)>0} g."""
+    cfg = syn.config("C4")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    g = plan.forward(cuda(syn.scene_blobs(geom), dev))
+    f = torch.ones(geom.m, dtype=torch.float32, device=dev)
+    plan.mlem(g, f, cfg.K)
+    gh = plan.forward(f)
+    assert bool((f >= 0).all())
+    s_g, s_gh = g.double().sum().item(), gh.double().sum().item()
+    assert abs(s_gh - s_g) <= 1e-4 * s_g
+
+
+def test_mlem_random_wrapping(ctis, oracle_lib, dev):
+    geom = syn.Geometry(33, 17, 6, 70, 45)
+    taps = syn.random_taps(geom, (2, 9), seed=77, region="any")
+    r, *_ = _mlem_case(ctis, oracle_lib, dev, geom, taps, 30, syn.scene_random(geom, seed=3, lo=0.1, zero_frac=0.1))
+    assert r <= MLEM_TOL, r
+
+
+def test_mlem_iters_zero_and_fixed_point(ctis, oracle_lib, dev):
+    cfg = syn.config("tiny")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    f = torch.rand(geom.m, device=dev) + 0.5
+    f0 = f.clone()
+    g = plan.forward(f)
+    plan.mlem(g, f, 0)
+    assert torch.equal(f, f0)
+    plan.mlem(g, f, 5)      # H f0 = g exactly up to fp32 -> stays put
+    assert rel(f.cpu().numpy(), f0.cpu().numpy()) <= 1e-5
+
+
+def test_mlem_zero_image_gives_zero(ctis, dev):
+    cfg = syn.config("tiny")
+    plan = ctis.Plan.from_geometry(cfg.geom, syn.paper_taps(cfg))
+    f = torch.ones(cfg.geom.m, device=dev)
+    plan.mlem(torch.zeros(cfg.geom.n, device=dev), f, 1)
+    assert bool((f == 0).all())
+
+
+def test_graph_and_direct_launch_identical(ctis, dev):
+    cfg = syn.config("C2")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    g = plan.forward(cuda(syn.scene_blobs(geom), dev))
+    f1 = torch.ones(geom.m, device=dev)
+    f2 = torch.ones(geom.m, device=dev)
+    plan.mlem(g, f1, 10)
+    plan.set_option(ctis.OPT_USE_GRAPH, 0)
+    plan.mlem(g, f2, 10)
+    assert torch.equal(f1, f2)
+
+
+# ------------------------------------------------------------------ batched frames (snapshot video)
+def test_batched_frames_equal_single_frame_runs(ctis, oracle_lib, dev):
+    cfg = syn.config("C2")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    F = 5
+    scenes = np.stack([syn.frame_scene(geom, i).reshape(-1) for i in range(F)])
+    g = plan.forward(cuda(scenes, dev).view(F, geom.m))
+    fb = torch.ones(F, geom.m, device=dev)
+    plan.mlem(g, fb, 20)
+    for i in range(F):
+        fi = torch.ones(geom.m, device=dev)
+        plan.mlem(g[i].contiguous(), fi, 20)
+        assert torch.equal(fi, fb[i])
+    want = oracle_lib.mlem(geom, taps, g[2].cpu().numpy(), np.ones(geom.m), 20)
+    assert rel(fb[2].cpu().numpy(), want) <= MLEM_TOL
+
+
+# ------------------------------------------------------------------ latency mode on one device (virtual shards)
+def test_band_shards_sum_to_full_forward_and_mlem(ctis, oracle_lib, dev):
+    from paper_2006_01573_b200 import distributed as dist_mod
+    cfg = syn.config("C2")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    full = ctis.Plan.from_geometry(geom, taps)
+    f = cuda(syn.scene_blobs(geom), dev)
+    parts = dist_mod.band_partition(geom.w, 3)
+    shards = [ctis.Plan.from_geometry(geom, taps, band_range=p) for p in parts]
+    ghat = sum(s.forward(f[p[0] * geom.ell:p[1] * geom.ell].contiguous()) for s, p in zip(shards, parts))
+    assert rel(ghat.cpu().numpy(), full.forward(f).cpu().numpy()) <= 1e-6
+    # MLEM with the all-reduce replaced by an on-device sum of the partials
+    g = full.forward(f)
+    f_full = torch.ones(geom.m, device=dev)
+    full.mlem(g, f_full, 20)
+    f_loc = [torch.ones(s.m, device=dev) for s in shards]
+    out = dist_mod.mlem_band_sharded_local(shards, g, f_loc, 20)
+    assert rel(torch.cat(out).cpu().numpy(), f_full.cpu().numpy()) <= 1e-4
+    with pytest.raises(ctis.CtisError):
+        shards[0].mlem(g, f_loc[0], 1)
+
+
+# ------------------------------------------------------------------ end-to-end host path
+def test_mlem_host_path_matches_device_path(ctis, dev):
+    cfg = syn.config("C2")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    g = plan.forward(cuda(syn.scene_blobs(geom), dev))
+    fd = torch.ones(geom.m, device=dev)
+    plan.mlem(g, fd, 15)
+    fh = np.ones(geom.m, np.float32)
+    plan.mlem_host(g.cpu().numpy(), fh, 15)
+    assert np.array_equal(fh, fd.cpu().numpy())
+
+
+# ------------------------------------------------------------------ error behaviour
+def test_error_codes(ctis, dev):
+    geom = syn.Geometry(8, 8, 2, 32, 32)
+    good = syn.random_taps(geom, 3, seed=1)
+
+    def make(**kw):
+        args = dict(tap_ptr=good.ptr, tap_offset=good.offset, tap_weight=good.weight)
+        args.update(kw)
+        return ctis.Plan(geom.a, geom.alpha, geom.w, geom.gamma, geom.xi, **args)
+
+    for kw, code in [
+        (dict(tap_offset=np.where(np.arange(6) == 0, geom.n, good.offset)), ctis.ERR_TAP),
+        (dict(tap_weight=np.where(np.arange(6) == 1, -1.0, good.weight).astype(np.float32)), ctis.ERR_TAP),
+        (dict(tap_weight=np.where(np.arange(6) == 1, np.nan, good.weight).astype(np.float32)), ctis.ERR_TAP),
+        (dict(tap_offset=np.array([5, 5, 7, 1, 2, 3])), ctis.ERR_TAP),
+        (dict(tap_ptr=np.array([0, 0, 6])), ctis.ERR_TAP),
+    ]:
+        with pytest.raises(ctis.CtisError) as ei:
+            make(**kw)
+        assert ei.value.status == code
+    with pytest.raises(ctis.CtisError) as ei:
+        ctis.Plan(8, 8, 2, 4, 32, good)
+    assert ei.value.status == ctis.ERR_DIMENSION
+    with pytest.raises(ctis.CtisError) as ei:
+        ctis.Plan(8, 8, 2, 32, 32, good, band_range=(1, 1))
+    assert ei.value.status == ctis.ERR_DIMENSION
+    plan = make()
+    g = torch.ones(geom.n, device=dev)
+    g[7] = float("nan")
+    with pytest.raises(ctis.CtisError) as ei:
+        plan.mlem(g, torch.ones(geom.m, device=dev), 3)
+    assert ei.value.status == ctis.ERR_DATA
+    f = torch.ones(geom.m, device=dev)
+    f[0] = -1
+    with pytest.raises(ctis.CtisError) as ei:
+        plan.mlem(torch.ones(geom.n, device=dev), f, 3)
+    assert ei.value.status == ctis.ERR_DATA
+    with pytest.raises(ctis.CtisError) as ei:
+        plan.mlem(torch.ones(geom.n, device=dev), torch.ones(geom.m, device=dev), -1)
+    assert ei.value.status == ctis.ERR_INVALID_ARGUMENT
