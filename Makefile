@@ -1,24 +1,39 @@
 # Builds the CUDA hot path (libctis.so, sm_100a) and the CPU oracle (liboracle.so).
 NVCC     ?= /usr/local/cuda/bin/nvcc
+BIN2C    ?= /usr/local/cuda/bin/bin2c
 PKG      := paper_2006_01573_b200
 ARCH     := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden -Xptxas -v \
-            --expt-relaxed-constexpr -Iinclude
-SRCS     := $(PKG)/csrc/ctis_api.cu $(PKG)/csrc/ctis_kernels.cu
-HDRS     := include/ctis.h $(PKG)/csrc/ctis_internal.h
-OBJS     := $(patsubst %.cu,build/%.o,$(SRCS))
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden \
+            --expt-relaxed-constexpr -Iinclude -Ibuild
+HDRS     := include/ctis.h $(PKG)/csrc/ctis_internal.h $(PKG)/csrc/ctis_kernels.h
 
 all: $(PKG)/libctis.so oracle/liboracle.so
 
-build/%.o: %.cu $(HDRS)
-	@mkdir -p $(dir $@)
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
+# Projection kernels: a standalone cubin, embedded and loaded once per plan tap page.
+build/ctis_tables.cubin: $(PKG)/csrc/ctis_tables.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Iinclude -cubin -Xptxas -v $< -o $@ 2> build/ctis_tables.ptxas.log \
+	  || (cat build/ctis_tables.ptxas.log; false)
 
-$(PKG)/libctis.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC -o $@.tmp $(OBJS) && mv $@.tmp $@
+build/ctis_tables_cubin.h: build/ctis_tables.cubin
+	$(BIN2C) --const --name ctis_tables_cubin $< > $@
+
+build/ctis_api.o: $(PKG)/csrc/ctis_api.cu build/ctis_tables_cubin.h $(HDRS)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+build/ctis_kernels.o: $(PKG)/csrc/ctis_kernels.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> build/ctis_kernels.ptxas.log || (cat build/ctis_kernels.ptxas.log; false)
+
+$(PKG)/libctis.so: build/ctis_api.o build/ctis_kernels.o
+	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC -o $@.tmp $^ && mv $@.tmp $@
 
 oracle/liboracle.so: oracle/ctis_oracle.c
 	gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -std=c99 -o $@ $<
+
+build/microbench: tools/microbench.cu
+	@mkdir -p build
+	$(NVCC) $(ARCH) -O3 -o $@ $<
 
 clean:
 	rm -rf build $(PKG)/libctis.so oracle/liboracle.so

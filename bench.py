@@ -110,7 +110,7 @@ def algorithmic(cfg, taps):
     m, n = g.m, g.n
     mT = int(taps.ptr[-1]) * g.ell            # sum over bands of T_lam * l = incidences per projection
     return {
-        "forward": {"bytes": 4 * m + 8 * n, "flops": 2 * mT + n},      # read f, read g, write r
+        "forward": {"bytes": 4 * m + 4 * n, "flops": 2 * mT},          # read f, write g_hat
         "back": {"bytes": 4 * n + 8 * m, "flops": 2 * mT + 2 * m},     # read r, read+write f
         "iteration": {"bytes": 12 * m + 12 * n, "flops": 4 * mT + n + 3 * m},
         "incidences": mT,
@@ -229,6 +229,7 @@ def main():
     for i in range(args.warmup):
         flush.zero_()
         one_step(fbufs[i])
+    launches_per_step = plan.last_launch_count() * (K if mode == "bands" else 1)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -257,19 +258,20 @@ def main():
     recon_total = args.steps * (frames * world if mode == "frames" else 1)
     iters_total = recon_total * K
     value = iters_total / (total_ms / 1e3)
-    launches = args.steps * K * (2 if mode == "frames" else 3)
+    launches = args.steps * launches_per_step
 
     # ---- per-kernel live timing for the roofline (CUDA events on the launching stream)
     alg = algorithmic(cfg, taps)
     hbm_peak, sm_max, peak_src = load_peaks()
+    fp32_peak = SM_COUNT * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
     kern = {}
     if rank == 0:
         reps = 20
         fk = fbufs[-1].view(-1)[:m_loc] if frames == 1 else fbufs[-1][0]
-        gk = g if frames == 1 else g[0]
         rk = ws.view(-1)[:geom.n]
+        scratch = torch.zeros(geom.n, dtype=torch.float32, device=dev)
         fu = fbufs[0].view(-1)[:m_loc]
-        for name, fn in (("forward_ratio", lambda: plan.forward_ratio(fk, gk, rk)),
+        for name, fn in (("forward", lambda: plan.forward_accumulate(fk, scratch)),
                          ("back_update", lambda: plan.back_update(rk, fu))):
             ts = []
             for _ in range(3):
@@ -285,15 +287,17 @@ def main():
     line = None
     if rank == 0:
         frac_w = (b1 - b0) / geom.w
-        fw_bytes, bk_bytes = alg["forward"]["bytes"], alg["back"]["bytes"]
-        fw_flops, bk_flops = alg["forward"]["flops"] * frac_w, alg["back"]["flops"] * frac_w
-        t_f, t_b = kern.get("forward_ratio", 0), kern.get("back_update", 0)
-        dom = "back_update" if t_b >= t_f else "forward_ratio"
-        t_dom = max(t_f, t_b)
-        dom_bytes = bk_bytes if dom == "back_update" else fw_bytes
-        dom_flops = bk_flops if dom == "back_update" else fw_flops
-        achieved = dom_bytes / t_dom / 1e9 if t_dom > 0 else None
-        fp32_peak = SM_COUNT * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+        work = {"forward": (alg["forward"]["bytes"], alg["forward"]["flops"] * frac_w),
+                "back_update": (alg["back"]["bytes"], alg["back"]["flops"] * frac_w)}
+        dom = max(kern, key=kern.get)
+        t_dom = kern[dom]
+        dom_bytes, dom_flops = work[dom]
+        t_hbm, t_alu = dom_bytes / (hbm_peak * 1e9), dom_flops / (fp32_peak * 1e12)
+        if t_hbm >= t_alu:
+            roof = {"bound": "hbm", "achieved": dom_bytes / t_dom / 1e9, "peak": hbm_peak, "unit": "GB/s"}
+        else:
+            roof = {"bound": "alu", "achieved": dom_flops / t_dom / 1e12, "peak": fp32_peak, "unit": "TFLOP/s"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
         traffic = None
         prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(prof):
@@ -302,6 +306,15 @@ def main():
             except Exception:
                 traffic = None
         it_ms = total_ms / (args.steps * K)
+        t_it_roof = max(alg["iteration"]["bytes"] / (hbm_peak * 1e9), alg["iteration"]["flops"] / (fp32_peak * 1e12))
+        roof.update({
+            "kernel": dom, "traffic": traffic, "peak_source": peak_src,
+            "alg_bytes_per_launch": dom_bytes, "alg_flops_per_launch": dom_flops,
+            "fp32_tflops_achieved": dom_flops / t_dom / 1e12, "fp32_peak_tflops": fp32_peak,
+            "hbm_gbs_achieved": dom_bytes / t_dom / 1e9,
+            "smem_operand_frac": (alg["incidences"] * frac_w * 4 / t_dom) / (SM_COUNT * 128 * sm_max * 1e6),
+            "iteration_roof_us": t_it_roof * 1e6,
+            "iteration_frac": (t_it_roof / (it_ms * 1e-3)) if mode == "frames" and frames == 1 else None})
         line = {
             "metric": "MLEM iterations/s", "value": value, "unit": "iterations/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -315,15 +328,7 @@ def main():
             "recon_per_s": recon_total / (total_ms / 1e3),
             "ms_per_iteration": it_ms,
             "kernels_ms": {k: v * 1e3 for k, v in kern.items()},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
-                         "peak_source": peak_src,
-                         "alg_bytes_per_launch": dom_bytes, "alg_flops_per_launch": dom_flops,
-                         "fp32_tflops_achieved": dom_flops / t_dom / 1e12 if t_dom > 0 else None,
-                         "fp32_peak_tflops": fp32_peak,
-                         "iteration_frac": (max(alg["iteration"]["bytes"] / (hbm_peak * 1e9),
-                                                alg["iteration"]["flops"] / (fp32_peak * 1e12))
-                                            / (it_ms * 1e-3)) if mode == "frames" and frames == 1 else None},
+            "roofline": roof,
             "clocks": clocks,
             "gpu_launches": launches,
         }

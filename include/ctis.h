@@ -125,6 +125,11 @@ CTIS_API ctis_status ctis_forward(ctis_plan plan, const float* f, float* g_hat, 
 CTIS_API ctis_status ctis_forward_batched(ctis_plan plan, const float* f, float* g_hat, int64_t frames,
                                  ctis_stream stream);
 
+/* g_hat += H f without clearing g_hat first (the forward kernels accumulate band-chunk
+ * partials with red.global.add): f[frames][m_local], g_hat[frames][n]. */
+CTIS_API ctis_status ctis_forward_accumulate(ctis_plan plan, const float* f, float* g_hat, int64_t frames,
+                                             ctis_stream stream);
+
 /* z = H^T r (Eqs. 14-17): r[n] -> z[m_local], overwritten. */
 CTIS_API ctis_status ctis_backproject(ctis_plan plan, const float* r, float* z, ctis_stream stream);
 

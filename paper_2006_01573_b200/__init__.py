@@ -37,6 +37,7 @@ _SIGS = {
     "ctis_workspace_bytes": ([_P, _i64], ctypes.c_size_t),
     "ctis_forward": ([_P, _P, _P, _P], _int),
     "ctis_forward_batched": ([_P, _P, _P, _i64, _P], _int),
+    "ctis_forward_accumulate": ([_P, _P, _P, _i64, _P], _int),
     "ctis_backproject": ([_P, _P, _P, _P], _int),
     "ctis_sensitivity": ([_P, _P, _P], _int),
     "ctis_mlem": ([_P, _P, _P, _int, _P, _P], _int),
@@ -170,6 +171,14 @@ class Plan:
         fp = _dev_ptr(f, self.m * frames, "f")
         gp = _dev_ptr(out, self.n * frames, "g_hat")
         _check(_lib.ctis_forward_batched(self._h, fp, gp, frames, _stream_handle(stream)), "ctis_forward")
+        return out
+
+    def forward_accumulate(self, f, out, stream=None):
+        """g_hat += H f (no clearing; the forward kernels accumulate with red.add)."""
+        frames = f.numel() // self.m
+        _check(_lib.ctis_forward_accumulate(self._h, _dev_ptr(f, self.m * frames, "f"),
+                                            _dev_ptr(out, self.n * frames, "g_hat"), frames,
+                                            _stream_handle(stream)), "ctis_forward_accumulate")
         return out
 
     def backproject(self, r, out=None, stream=None):

@@ -1,10 +1,11 @@
-// ctis_api.cu — the C ABI of libctis (include/ctis.h): plan builder, validation,
-// stream-ordered entry points, CUDA-graph replay of the MLEM iterations.
+// ctis_api.cu — the C ABI of libctis (include/ctis.h): plan builder (tap validation,
+// mode clustering, __constant__ tap pages), stream-ordered entry points, CUDA-graph
+// replay of the MLEM iterations.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
-#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -14,6 +15,8 @@
 
 #include "../../include/ctis.h"
 #include "ctis_internal.h"
+#include "ctis_kernels.h"
+#include "ctis_tables_cubin.h"  // generated: unsigned char ctis_tables_cubin[] (bin2c)
 
 using namespace ctis;
 
@@ -31,9 +34,9 @@ ctis_status cuda_fail(cudaError_t e, const char* where) {
   return e == cudaErrorMemoryAllocation ? CTIS_ERR_OUT_OF_MEMORY : CTIS_ERR_CUDA;
 }
 
-#define CTIS_CUDA(call, where)                    \
-  do {                                            \
-    cudaError_t e__ = (call);                     \
+#define CTIS_CUDA(call, where)                            \
+  do {                                                    \
+    cudaError_t e__ = (call);                             \
     if (e__ != cudaSuccess) return cuda_fail(e__, where); \
   } while (0)
 
@@ -61,24 +64,34 @@ struct GraphKey {
   }
 };
 
+// One 64 KB __constant__ page of tap tables and the library instance that owns it.
+struct Page {
+  bool forward = true;
+  int nchunks = 0;
+  int max_tiles = 0;
+  int max_modes = 0;
+  std::vector<uint32_t> words;
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+};
+
+constexpr int kPageHeader = 64;  // word 0 = nchunks, words 1..63 = chunk descriptor offsets
+
 }  // namespace
 
 struct ctis_plan_s {
   int device = 0;
-  Dims d{};
-  int64_t band_begin = 0, band_end = 0, w_total = 0, total_taps = 0;
-  bool shard = false;
-  bool validate = true;
-  bool use_graph = true;
-  DevTables t{};
-  std::vector<void*> allocations;
+  int a = 0, alpha = 0, w = 0, gamma = 0, xi = 0, n = 0, ell = 0, m = 0;
+  int64_t band_begin = 0, band_end = 0, total_taps = 0;
+  bool shard = false, validate = true, use_graph = true;
+  bool vec_f = false, vec_b = false;
+  std::vector<Page> fwd, back;
+  float* d_hband = nullptr;
   int* d_flag = nullptr;
-  // host-buffer path
-  float* d_g = nullptr;
+  float* d_g = nullptr;  // host-buffer path
   float* d_f = nullptr;
   void* d_ws = nullptr;
   int64_t host_frames = 0;
-  // graphs
   cudaStream_t side = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
@@ -91,51 +104,324 @@ struct ctis_plan_s {
     if (side) cudaStreamDestroy(side);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
-    for (void* p : allocations) cudaFree(p);
-    if (d_g) cudaFree(d_g);
-    if (d_f) cudaFree(d_f);
-    if (d_ws) cudaFree(d_ws);
+    for (auto* pages : {&fwd, &back})
+      for (Page& p : *pages)
+        if (p.lib) cudaLibraryUnload(p.lib);
+    for (void* p : {(void*)d_hband, (void*)d_flag, (void*)d_g, (void*)d_f, d_ws})
+      if (p) cudaFree(p);
   }
 };
 
 namespace {
 
-template <typename T>
-ctis_status upload(ctis_plan p, const std::vector<T>& v, const T** out, const char* what) {
-  void* ptr = nullptr;
-  size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
-  CTIS_CUDA(cudaMalloc(&ptr, bytes), what);
-  p->allocations.push_back(ptr);
-  if (!v.empty()) CTIS_CUDA(cudaMemcpy(ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), what);
-  *out = static_cast<const T*>(ptr);
+// ------------------------------------------------------------------------------------------------
+// Mode clustering.  Within a chunk of consecutive bands, taps that drift together from band to
+// band (the same diffraction order at slightly different dispersion) are grouped into a "mode"
+// with a reference offset o_ref; every tap is then o = o_ref + dr + gamma*dc with a small 2-D
+// shift (dr, dc).  Any assignment is exact (the identity is integer arithmetic); clustering only
+// decides how much shared-memory window each kernel stages.
+struct TapXY {
+  int dr, dc;  // o = dr + gamma * dc, 0 <= dr < gamma
+  float w;
+};
+struct ModeTap {
+  int b, dr, dc;
+  float w;
+};
+struct Mode {
+  int ref_dr, ref_dc;
+  int lo_dr, lo_dc, hi_dr, hi_dc;  // last matched position below / above the reference band
+  std::vector<ModeTap> taps;
+  std::vector<char> has;
+};
+
+constexpr int kModeTrack = 3;   // max band-to-band move of a mode (pixels, Chebyshev)
+constexpr int kModeSpan = 12;   // max |shift| of a tap from its mode reference (pixels)
+
+std::vector<Mode> cluster_modes(const std::vector<std::vector<TapXY>>& bands) {
+  const int nb = (int)bands.size();
+  const int bref = (nb - 1) / 2;
+  std::vector<Mode> modes;
+  auto add_mode = [&](int b, const TapXY& t) {
+    Mode md;
+    md.ref_dr = md.lo_dr = md.hi_dr = t.dr;
+    md.ref_dc = md.lo_dc = md.hi_dc = t.dc;
+    md.has.assign(nb, 0);
+    md.has[b] = 1;
+    md.taps.push_back(ModeTap{b, t.dr, t.dc, t.w});
+    modes.push_back(std::move(md));
+  };
+  for (const TapXY& t : bands[bref]) add_mode(bref, t);
+  std::vector<int> order;
+  for (int d = 1; d < nb; ++d) {
+    if (bref + d < nb) order.push_back(bref + d);
+    if (bref - d >= 0) order.push_back(bref - d);
+  }
+  for (int b : order) {
+    const bool up = b > bref;
+    for (const TapXY& t : bands[b]) {
+      int best = -1, bestd = INT_MAX;
+      for (int i = 0; i < (int)modes.size(); ++i) {
+        Mode& md = modes[i];
+        if (md.has[b]) continue;
+        const int ldr = up ? md.hi_dr : md.lo_dr, ldc = up ? md.hi_dc : md.lo_dc;
+        const int d = std::max(std::abs(t.dr - ldr), std::abs(t.dc - ldc));
+        const int s = std::max(std::abs(t.dr - md.ref_dr), std::abs(t.dc - md.ref_dc));
+        if (d <= kModeTrack && s <= kModeSpan && d < bestd) {
+          best = i;
+          bestd = d;
+        }
+      }
+      if (best < 0) {
+        add_mode(b, t);
+        continue;
+      }
+      Mode& md = modes[best];
+      md.has[b] = 1;
+      md.taps.push_back(ModeTap{b, t.dr, t.dc, t.w});
+      if (up) {
+        md.hi_dr = t.dr;
+        md.hi_dc = t.dc;
+      } else {
+        md.lo_dr = t.dr;
+        md.lo_dc = t.dc;
+      }
+    }
+  }
+  return modes;
+}
+
+inline int mod4(long long x) { return (int)(((x % 4) + 4) % 4); }
+inline int round4(int x) { return (x + 3) & ~3; }
+inline uint32_t fbits(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  return u;
+}
+
+// Forward chunk descriptor for bands [b0, b0+nb) (local) and the given modes.
+bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const Mode*>& ms, bool vec,
+                  std::vector<uint32_t>& out, int& tiles) {
+  const int nm = (int)ms.size();
+  std::vector<int> rmin(nb, INT_MAX), rmax(nb, INT_MIN), cmin(nb, INT_MAX), cmax(nb, INT_MIN);
+  int Rmin = INT_MAX, Rmax = INT_MIN, Cmin = INT_MAX, Cmax = INT_MIN;
+  for (const Mode* md : ms)
+    for (const ModeTap& t : md->taps) {
+      const int dr = t.dr - md->ref_dr, dc = t.dc - md->ref_dc;
+      rmin[t.b] = std::min(rmin[t.b], dr);
+      rmax[t.b] = std::max(rmax[t.b], dr);
+      cmin[t.b] = std::min(cmin[t.b], dc);
+      cmax[t.b] = std::max(cmax[t.b], dc);
+      Rmin = std::min(Rmin, dr);
+      Rmax = std::max(Rmax, dr);
+      Cmin = std::min(Cmin, dc);
+      Cmax = std::max(Cmax, dc);
+    }
+  if (Rmin == INT_MAX) return true;  // no taps: nothing to emit
+  const int u_r0 = Rmin, u_c0 = Cmin;
+  const int tiles_r = (P.a + Rmax - Rmin + kFwdTR - 1) / kFwdTR;
+  const int tiles_c = (P.alpha + Cmax - Cmin + kFwdTC - 1) / kFwdTC;
+  out.assign(kDescHeader + nm + 4 * nb + 2 * nb * nm, 0u);
+  out[0] = (uint32_t)b0;
+  out[1] = (uint32_t)nb;
+  out[2] = (uint32_t)nm;
+  out[3] = (uint32_t)u_r0;
+  out[4] = (uint32_t)u_c0;
+  out[5] = (uint32_t)tiles_r;
+  out[6] = (uint32_t)tiles_c;
+  for (int c = 0; c < nm; ++c) out[kDescHeader + c] = (uint32_t)(ms[c]->ref_dr + P.gamma * ms[c]->ref_dc);
+  const int BI = kDescHeader + nm, TP = BI + 4 * nb;
+  std::vector<int> WRs(nb, 4), lead(nb, 0);
+  for (int b = 0; b < nb; ++b) {
+    if (rmin[b] == INT_MAX) {  // band without taps in this pass: empty window
+      out[BI + 4 * b + 2] = 4;
+      out[BI + 4 * b + 3] = 0;
+      continue;
+    }
+    lead[b] = vec ? mod4((long long)u_r0 - rmax[b]) : 0;
+    int WR = kFwdTR + rmax[b] - rmin[b] + lead[b];
+    if (vec) WR = round4(WR);
+    const int WC = kFwdTC + cmax[b] - cmin[b];
+    if (WR * WC > kFwdWinFloats) return false;
+    WRs[b] = WR;
+    out[BI + 4 * b + 0] = (uint32_t)(-rmax[b] - lead[b]);
+    out[BI + 4 * b + 1] = (uint32_t)(-cmax[b]);
+    out[BI + 4 * b + 2] = (uint32_t)WR;
+    out[BI + 4 * b + 3] = (uint32_t)WC;
+  }
+  for (int c = 0; c < nm; ++c)
+    for (const ModeTap& t : ms[c]->taps) {
+      const int dr = t.dr - ms[c]->ref_dr, dc = t.dc - ms[c]->ref_dc;
+      const int off = (rmax[t.b] + lead[t.b] - dr) + WRs[t.b] * (cmax[t.b] - dc);
+      out[TP + 2 * (t.b * nm + c)] = (uint32_t)off;
+      out[TP + 2 * (t.b * nm + c) + 1] = fbits(t.w);
+    }
+  tiles = tiles_r * tiles_c;
+  return true;
+}
+
+// Back chunk descriptor for bands [b0, b0+nb) (local) and all modes of the chunk.
+bool back_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<Mode>& ms, const std::vector<float>& invh,
+               bool vec, std::vector<uint32_t>& out, int& tiles) {
+  const int nm = (int)ms.size();
+  out.assign(kDescHeader + 4 * nm + 2 * nm * nb + nb, 0u);
+  const int tiles_r = (P.a + kBackTR - 1) / kBackTR, tiles_c = (P.alpha + kBackTC - 1) / kBackTC;
+  out[0] = (uint32_t)b0;
+  out[1] = (uint32_t)nb;
+  out[2] = (uint32_t)nm;
+  out[3] = (uint32_t)tiles_r;
+  out[4] = (uint32_t)tiles_c;
+  const int MI = kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * nb;
+  for (int c = 0; c < nm; ++c) {
+    const Mode& md = ms[c];
+    int rmin = INT_MAX, rmax = INT_MIN, cmin = INT_MAX, cmax = INT_MIN;
+    for (const ModeTap& t : md.taps) {
+      rmin = std::min(rmin, t.dr - md.ref_dr);
+      rmax = std::max(rmax, t.dr - md.ref_dr);
+      cmin = std::min(cmin, t.dc - md.ref_dc);
+      cmax = std::max(cmax, t.dc - md.ref_dc);
+    }
+    const long long oref = (long long)md.ref_dr + (long long)P.gamma * md.ref_dc;
+    const long long B0 = oref + rmin + (long long)P.gamma * cmin;
+    const int lead = vec ? mod4(B0) : 0;
+    long long Bm = (B0 - lead) % P.n;
+    if (Bm < 0) Bm += P.n;
+    int WR = kBackTR + rmax - rmin + lead;
+    if (vec) WR = round4(WR);
+    const int WC = kBackTC + cmax - cmin;
+    if (WR * WC > kBackWinFloats) return false;
+    out[MI + 4 * c + 0] = (uint32_t)Bm;
+    out[MI + 4 * c + 1] = (uint32_t)WR;
+    out[MI + 4 * c + 2] = (uint32_t)WC;
+    for (const ModeTap& t : md.taps) {
+      const int dr = t.dr - md.ref_dr, dc = t.dc - md.ref_dc;
+      out[TP + 2 * (c * nb + t.b)] = (uint32_t)((dr - rmin + lead) + WR * (dc - cmin));
+      out[TP + 2 * (c * nb + t.b) + 1] = fbits(t.w);
+    }
+  }
+  for (int b = 0; b < nb; ++b) out[IH + b] = fbits(invh[b0 + b]);
+  tiles = tiles_r * tiles_c;
+  return true;
+}
+
+// Append descriptors to pages (<= 64 KB and <= 63 chunks each).
+void pack_pages(std::vector<Page>& pages, bool forward, const std::vector<std::vector<uint32_t>>& descs,
+                const std::vector<int>& tiles, const std::vector<int>& modes) {
+  Page cur;
+  auto flush = [&]() {
+    if (cur.nchunks) pages.push_back(std::move(cur));
+    cur = Page();
+  };
+  for (size_t i = 0; i < descs.size(); ++i) {
+    if (cur.nchunks == 0) {
+      cur.forward = forward;
+      cur.words.assign(kPageHeader, 0u);
+    }
+    if (cur.nchunks == kPageHeader - 1 || cur.words.size() + descs[i].size() > (size_t)kPageWords) {
+      flush();
+      cur.forward = forward;
+      cur.words.assign(kPageHeader, 0u);
+    }
+    cur.words[1 + cur.nchunks] = (uint32_t)cur.words.size();
+    cur.words.insert(cur.words.end(), descs[i].begin(), descs[i].end());
+    cur.nchunks++;
+    cur.words[0] = (uint32_t)cur.nchunks;
+    cur.max_tiles = std::max(cur.max_tiles, tiles[i]);
+    cur.max_modes = std::max(cur.max_modes, modes[i]);
+  }
+  flush();
+}
+
+const void* tables_image() {
+  // 8-byte aligned copy of the embedded cubin (bin2c emits a byte array).
+  static std::vector<uint64_t> img = [] {
+    std::vector<uint64_t> v((sizeof(ctis_tables_cubin) + 7) / 8, 0);
+    std::memcpy(v.data(), ctis_tables_cubin, sizeof(ctis_tables_cubin));
+    return v;
+  }();
+  return img.data();
+}
+
+ctis_status load_page(Page& pg, bool vec) {
+  CTIS_CUDA(cudaLibraryLoadData(&pg.lib, tables_image(), nullptr, nullptr, 0, nullptr, nullptr, 0),
+            "cudaLibraryLoadData (tap page)");
+  void* dptr = nullptr;
+  size_t bytes = 0;
+  CTIS_CUDA(cudaLibraryGetGlobal(&dptr, &bytes, pg.lib, "c_tab"), "cudaLibraryGetGlobal(c_tab)");
+  if (pg.words.size() * 4 > bytes) return fail(CTIS_ERR_INVALID_ARGUMENT, "tap page overflow");
+  CTIS_CUDA(cudaMemcpy(dptr, pg.words.data(), pg.words.size() * 4, cudaMemcpyHostToDevice), "upload tap page");
+  std::string name;
+  if (pg.forward) {
+    const int mm = pg.max_modes <= 16 ? 16 : pg.max_modes <= 32 ? 32 : pg.max_modes <= 64 ? 64 : 96;
+    name = "ctis_fwd_m" + std::to_string(mm) + (vec ? "_v" : "_s");
+  } else {
+    name = std::string("ctis_back") + (vec ? "_v" : "_s");
+  }
+  CTIS_CUDA(cudaLibraryGetKernel(&pg.kern, pg.lib, name.c_str()), "cudaLibraryGetKernel");
   return CTIS_OK;
 }
 
-// One rectangle piece of a tap: field-stop rows [r0,r1) x cols [c0,c1) map to FPA (r+sr, c+sc).
-struct Piece {
-  int lam;
-  float w;
-  int r0, r1, c0, c1;
-  int sr, sc;
-};
-
-// Split the 1-D cyclic shift by o (Eq. 7) into <= 4 pure 2-D translations.
-void decompose_tap(const Dims& d, int lam, int64_t o, float w, std::vector<Piece>& out) {
-  const int dr = (int)(o % d.gamma), dc = (int)(o / d.gamma);
-  for (int carry = 0; carry < 2; ++carry) {
-    const int r0 = carry ? std::max(0, d.gamma - dr) : 0;
-    const int r1 = carry ? d.a : std::min(d.a, d.gamma - dr);
-    if (r0 >= r1) continue;
-    const int sr = carry ? dr - d.gamma : dr;
-    const int dc1 = dc + carry;  // <= xi
-    for (int wrap = 0; wrap < 2; ++wrap) {
-      const int c0 = wrap ? std::max(0, d.xi - dc1) : 0;
-      const int c1 = wrap ? d.alpha : std::min(d.alpha, d.xi - dc1);
-      if (c0 >= c1) continue;
-      const int sc = wrap ? dc1 - d.xi : dc1;
-      out.push_back(Piece{lam, w, r0, r1, c0, c1, sr, sc});
+ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& bands, const std::vector<float>& invh) {
+  P.vec_f = (P.a % 4 == 0);
+  P.vec_b = (P.gamma % 4 == 0);
+  // ---- forward: chunks of kFwdBands bands, modes split into passes of <= 96
+  {
+    std::vector<std::vector<uint32_t>> descs;
+    std::vector<int> tiles, modes;
+    for (int b0 = 0; b0 < P.w; b0 += kFwdBands) {
+      const int nb = std::min(kFwdBands, P.w - b0);
+      std::vector<std::vector<TapXY>> cb(bands.begin() + b0, bands.begin() + b0 + nb);
+      std::vector<Mode> ms = cluster_modes(cb);
+      for (size_t s = 0; s < ms.size(); s += 96) {
+        std::vector<const Mode*> pass;
+        for (size_t c = s; c < std::min(ms.size(), s + 96); ++c) pass.push_back(&ms[c]);
+        std::vector<uint32_t> d;
+        int t = 0;
+        if (!forward_desc(P, b0, nb, pass, P.vec_f, d, t)) return fail(CTIS_ERR_TAP, "forward window overflow");
+        if (d.empty()) continue;
+        descs.push_back(std::move(d));
+        tiles.push_back(t);
+        modes.push_back((int)pass.size());
+      }
     }
+    pack_pages(P.fwd, true, descs, tiles, modes);
   }
+  // ---- back: chunks of up to kBackBands bands (fewer if a descriptor would not fit a page)
+  {
+    std::vector<std::vector<uint32_t>> descs;
+    std::vector<int> tiles, modes;
+    int b0 = 0;
+    while (b0 < P.w) {
+      int nb = std::min(kBackBands, P.w - b0);
+      for (;;) {
+        std::vector<std::vector<TapXY>> cb(bands.begin() + b0, bands.begin() + b0 + nb);
+        std::vector<Mode> ms = cluster_modes(cb);
+        std::vector<uint32_t> d;
+        int t = 0;
+        if (!back_desc(P, b0, nb, ms, invh, P.vec_b, d, t)) return fail(CTIS_ERR_TAP, "back window overflow");
+        if ((int)d.size() + kPageHeader <= kPageWords || nb == 1) {
+          if ((int)d.size() + kPageHeader > kPageWords)
+            return fail(CTIS_ERR_TAP, "band has too many taps for one 64 KB tap page");
+          descs.push_back(std::move(d));
+          tiles.push_back(t);
+          modes.push_back((int)ms.size());
+          break;
+        }
+        nb = (nb + 1) / 2;
+      }
+      b0 += nb;
+    }
+    pack_pages(P.back, false, descs, tiles, modes);
+  }
+  for (Page& pg : P.fwd) {
+    ctis_status st = load_page(pg, P.vec_f);
+    if (st) return st;
+  }
+  for (Page& pg : P.back) {
+    ctis_status st = load_page(pg, P.vec_b);
+    if (st) return st;
+  }
+  return CTIS_OK;
 }
 
 ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi, const int64_t* tap_ptr,
@@ -148,20 +434,21 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
     return fail(CTIS_ERR_DIMENSION, "a, alpha, w, gamma, xi must be >= 1");
   if (gamma < a || xi < alpha) return fail(CTIS_ERR_DIMENSION, "field stop must fit the FPA (gamma >= a, xi >= alpha)");
   const int64_t n = gamma * xi, ell = a * alpha;
-  if (n >= (int64_t(1) << 31) || ell * w >= (int64_t(1) << 31))
-    return fail(CTIS_ERR_DIMENSION, "n and m must be < 2^31");
+  if (n >= (int64_t(1) << 31) || ell * w >= (int64_t(1) << 31)) return fail(CTIS_ERR_DIMENSION, "n and m must be < 2^31");
   if (b0 < 0 || b1 > w || b0 >= b1) return fail(CTIS_ERR_DIMENSION, "band range must be a non-empty subrange of [0, w)");
-  // --- taps: CSR, range, weights, duplicates (validated over ALL bands, shard or not)
   if (tap_ptr[0] != 0) return fail(CTIS_ERR_TAP, "tap_ptr[0] must be 0");
+  std::vector<float> hband;
   for (int64_t l = 0; l < w; ++l) {
-    if (tap_ptr[l + 1] <= tap_ptr[l]) return fail(CTIS_ERR_TAP, "band " + std::to_string(l) + " has no taps (or tap_ptr decreases)");
+    if (tap_ptr[l + 1] <= tap_ptr[l])
+      return fail(CTIS_ERR_TAP, "band " + std::to_string(l) + " has no taps (or tap_ptr decreases)");
     std::vector<int64_t> offs;
     double hs = 0.0;
     for (int64_t t = tap_ptr[l]; t < tap_ptr[l + 1]; ++t) {
       if (tap_offset[t] < 0 || tap_offset[t] >= n)
         return fail(CTIS_ERR_TAP, "tap offset outside [0, n) in band " + std::to_string(l));
       const float wt = tap_weight[t];
-      if (!(wt > 0.f) || !std::isfinite(wt)) return fail(CTIS_ERR_TAP, "tap weight not finite and > 0 in band " + std::to_string(l));
+      if (!(wt > 0.f) || !std::isfinite(wt))
+        return fail(CTIS_ERR_TAP, "tap weight not finite and > 0 in band " + std::to_string(l));
       offs.push_back(tap_offset[t]);
       hs += wt;
     }
@@ -169,6 +456,7 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
     if (std::adjacent_find(offs.begin(), offs.end()) != offs.end())
       return fail(CTIS_ERR_TAP, "duplicate tap offset in band " + std::to_string(l));
     if (!((float)hs > 0.f) || !std::isfinite((float)hs)) return fail(CTIS_ERR_ZERO_SENSITIVITY, "h_lambda not > 0");
+    hband.push_back((float)hs);
   }
   int ndev = 0;
   CTIS_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
@@ -183,93 +471,46 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
   p->shard = shard;
   p->band_begin = b0;
   p->band_end = b1;
-  p->w_total = w;
-  const int wl = (int)(b1 - b0);
-  p->d = Dims{(int)a, (int)alpha, wl, (int)gamma, (int)xi, (int)n, (int)ell, (int)(ell * wl)};
-  const Dims& d = p->d;
-
-  // --- per-band tables (local band index lam = l - b0), sorted by offset
-  std::vector<int> band_ptr4(wl + 1, 0), band_cnt(wl, 0), toff;
-  std::vector<float> tw, invh(wl), hb(wl);
-  std::vector<Piece> pieces;
-  for (int lam = 0; lam < wl; ++lam) {
+  p->a = (int)a;
+  p->alpha = (int)alpha;
+  p->w = (int)(b1 - b0);
+  p->gamma = (int)gamma;
+  p->xi = (int)xi;
+  p->n = (int)n;
+  p->ell = (int)ell;
+  p->m = (int)(ell * p->w);
+  std::vector<std::vector<TapXY>> bands(p->w);
+  std::vector<float> invh(p->w), hloc(p->w);
+  for (int lam = 0; lam < p->w; ++lam) {
     const int64_t l = b0 + lam;
-    std::vector<std::pair<int64_t, float>> bt;
     double hs = 0.0;
+    std::vector<std::pair<int64_t, float>> bt;
     for (int64_t t = tap_ptr[l]; t < tap_ptr[l + 1]; ++t) {
       bt.emplace_back(tap_offset[t], tap_weight[t]);
       hs += tap_weight[t];
     }
     std::sort(bt.begin(), bt.end());
-    band_ptr4[lam] = (int)toff.size();
-    band_cnt[lam] = (int)bt.size();
-    for (auto& x : bt) {
-      toff.push_back((int)x.first);
-      tw.push_back(x.second);
-      decompose_tap(d, lam, x.first, x.second, pieces);
-    }
-    while (toff.size() % 4) {
-      toff.push_back(0);
-      tw.push_back(0.f);
-    }
-    hb[lam] = (float)hs;
+    for (auto& x : bt) bands[lam].push_back(TapXY{(int)(x.first % gamma), (int)(x.first / gamma), x.second});
     invh[lam] = (float)(1.0 / hs);
+    hloc[lam] = hband[l];
     p->total_taps += (int64_t)bt.size();
   }
-  band_ptr4[wl] = (int)toff.size();
-
-  // --- forward tile binning: CSR of FwdEntry per FPA tile
-  const int tiles_r = (d.gamma + kFwdTileR - 1) / kFwdTileR, tiles_c = (d.xi + kFwdTileC - 1) / kFwdTileC;
-  const int ntiles = tiles_r * tiles_c;
-  std::vector<int> cnt(ntiles + 1, 0);
-  auto for_each_tile = [&](const Piece& pc, auto&& fn) {
-    const int R0 = pc.r0 + pc.sr, R1 = pc.r1 + pc.sr, C0 = pc.c0 + pc.sc, C1 = pc.c1 + pc.sc;
-    for (int tc = C0 / kFwdTileC; tc <= (C1 - 1) / kFwdTileC; ++tc)
-      for (int tr = R0 / kFwdTileR; tr <= (R1 - 1) / kFwdTileR; ++tr) fn(tr, tc, R0, R1, C0, C1);
-  };
-  for (const Piece& pc : pieces)
-    for_each_tile(pc, [&](int tr, int tc, int, int, int, int) { cnt[tc * tiles_r + tr + 1]++; });
-  for (int i = 0; i < ntiles; ++i) cnt[i + 1] += cnt[i];
-  std::vector<FwdEntry> ent(cnt[ntiles]);
-  std::vector<int> fill(cnt.begin(), cnt.end() - 1);
-  for (const Piece& pc : pieces) {
-    for_each_tile(pc, [&](int tr, int tc, int R0, int R1, int C0, int C1) {
-      const int tR0 = tr * kFwdTileR, tR1 = tR0 + kFwdTileR, tC0 = tc * kFwdTileC, tC1 = tC0 + kFwdTileC;
-      FwdEntry e{};
-      e.base = pc.lam * d.ell - pc.sr - d.a * pc.sc;
-      e.w = pc.w;
-      e.R0 = std::max(R0, tR0);
-      e.R1 = std::min(R1, tR1);
-      e.C0 = std::max(C0, tC0);
-      e.C1 = std::min(C1, tC1);
-      e.full = (e.R0 == tR0 && e.R1 == tR1 && e.C0 == tC0 && e.C1 == tC1 && tR1 <= d.gamma && tC1 <= d.xi) ? 1 : 0;
-      ent[fill[tc * tiles_r + tr]++] = e;
-    });
+  ctis_status st = build_tables(*p, bands, invh);
+  cudaError_t e = cudaSuccess;
+  if (!st) {
+    e = cudaMalloc(&p->d_hband, sizeof(float) * p->w);
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_hband, hloc.data(), sizeof(float) * p->w, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_flag, sizeof(int));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming);
+    if (e != cudaSuccess) st = cuda_fail(e, "plan scratch");
   }
-
-  ctis_status st;
-  if ((st = upload(p, ent, &p->t.fwd_entries, "upload fwd entries")) ||
-      (st = upload(p, cnt, &p->t.fwd_tile_ptr, "upload tile ptr")) ||
-      (st = upload(p, band_ptr4, &p->t.band_ptr4, "upload band ptr")) ||
-      (st = upload(p, band_cnt, &p->t.band_cnt, "upload band cnt")) ||
-      (st = upload(p, toff, &p->t.tap_off, "upload tap offsets")) ||
-      (st = upload(p, tw, &p->t.tap_w, "upload tap weights")) ||
-      (st = upload(p, invh, &p->t.inv_h, "upload inv_h")) || (st = upload(p, hb, &p->t.h, "upload h"))) {
+  if (st) {
     std::string msg = g_last_error;
     delete p;
     return fail(st, msg);
   }
-  p->t.tiles_r = tiles_r;
-  p->t.tiles_c = tiles_c;
-  cudaError_t e = cudaMalloc(&p->d_flag, sizeof(int));
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming);
-  if (e != cudaSuccess) {
-    delete p;
-    return cuda_fail(e, "plan scratch");
-  }
-  p->allocations.push_back(p->d_flag);
   *out = p;
   g_last_error.clear();
   return CTIS_OK;
@@ -285,74 +526,119 @@ ctis_status check_ptrs(std::initializer_list<const void*> ptrs) {
   return CTIS_OK;
 }
 
-ctis_status validate_data(ctis_plan p, const float* g, const float* f, int64_t frames, cudaStream_t s) {
-  CTIS_CUDA(cudaMemsetAsync(p->d_flag, 0, sizeof(int), s), "validate memset");
-  CTIS_CUDA(launch_validate(g, (int64_t)p->d.n * frames, p->d_flag, s), "validate g");
-  CTIS_CUDA(launch_validate(f, (int64_t)p->d.m * frames, p->d_flag, s), "validate f0");
+ctis_status check_frames(int64_t frames) {
+  if (frames < 1 || frames > 65535) return fail(CTIS_ERR_INVALID_ARGUMENT, "frames must be in [1, 65535]");
+  return CTIS_OK;
+}
+
+// ---- launches --------------------------------------------------------------------------------
+cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const float* src, float* dst,
+                         long long src_frame, long long dst_frame, int frames, int mode, cudaStream_t s,
+                         int64_t* count) {
+  TabArgs A{src, dst, src_frame, dst_frame, P.a, P.alpha, P.gamma, P.n, P.ell, mode};
+  for (const Page& pg : pages) {
+    dim3 grid(pg.max_tiles, pg.nchunks, frames);
+    void* args[] = {&A};
+    const int threads = pg.forward ? kFwdThreads : kBackThreads;
+    const size_t smem = 2 * sizeof(float) * (pg.forward ? kFwdWinFloats : kBackWinFloats);
+    cudaError_t e = cudaLaunchKernel((const void*)pg.kern, grid, dim3(threads), args, smem, s);
+    if (e != cudaSuccess) return e;
+    if (count) ++*count;
+  }
+  return cudaSuccess;
+}
+
+// g_hat (accumulated with red.add: must be zero on entry) += H f
+cudaError_t enqueue_forward(ctis_plan_s& P, const float* f, float* ghat, int frames, cudaStream_t s, int64_t* cnt) {
+  return launch_pages(P, P.fwd, f, ghat, P.m, P.n, frames, 0, s, cnt);
+}
+
+cudaError_t enqueue_back(ctis_plan_s& P, const float* r, float* fz, int frames, int mode, cudaStream_t s,
+                         int64_t* cnt) {
+  return launch_pages(P, P.back, r, fz, P.n, P.m, frames, mode, s, cnt);
+}
+
+ctis_status validate_data(ctis_plan_s& P, const float* g, const float* f, int64_t frames, cudaStream_t s) {
+  CTIS_CUDA(cudaMemsetAsync(P.d_flag, 0, sizeof(int), s), "validate memset");
+  CTIS_CUDA(launch_validate(g, (long long)P.n * frames, P.d_flag, s), "validate g");
+  CTIS_CUDA(launch_validate(f, (long long)P.m * frames, P.d_flag, s), "validate f0");
   int flag = 0;
-  CTIS_CUDA(cudaMemcpyAsync(&flag, p->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s), "validate copy");
+  CTIS_CUDA(cudaMemcpyAsync(&flag, P.d_flag, sizeof(int), cudaMemcpyDeviceToHost, s), "validate copy");
   CTIS_CUDA(cudaStreamSynchronize(s), "validate sync");
   if (flag) return fail(CTIS_ERR_DATA, "g or f0 contains a negative, NaN or Inf value");
   return CTIS_OK;
 }
 
-// Enqueue `iters` MLEM iterations (2 kernels each) on stream s.
-cudaError_t enqueue_iterations(ctis_plan p, const float* g, float* f, float* r, int frames, int iters,
-                               cudaStream_t s) {
-  for (int k = 0; k < iters; ++k) {
-    cudaError_t e = launch_forward(p->d, p->t, f, g, r, frames, /*ratio=*/true, s);
-    if (e != cudaSuccess) return e;
-    e = launch_back(p->d, p->t, r, f, frames, kBackUpdate, s);
-    if (e != cudaSuccess) return e;
+// One MLEM reconstruction: ws = [A: g_hat accumulator, frames*n][B: r, frames*n].
+cudaError_t enqueue_mlem(ctis_plan_s& P, const float* g, float* f, float* ws, int frames, int iters, cudaStream_t s,
+                         int64_t* cnt) {
+  float* A = ws;
+  float* B = ws + (size_t)P.n * frames;
+  const long long count = (long long)P.n * frames;
+  cudaError_t e = cudaMemsetAsync(A, 0, sizeof(float) * (size_t)count, s);
+  for (int k = 0; k < iters && e == cudaSuccess; ++k) {
+    e = enqueue_forward(P, f, A, frames, s, cnt);
+    if (e == cudaSuccess) {
+      e = launch_ratio(g, A, B, count, /*zero_ghat=*/true, s);
+      ++*cnt;
+    }
+    if (e == cudaSuccess) e = enqueue_back(P, B, f, frames, 1, s, cnt);
   }
-  return cudaSuccess;
+  return e;
 }
 
-ctis_status run_mlem(ctis_plan p, const float* g, float* f, int64_t frames, int iters, void* ws, cudaStream_t s) {
-  if (p->shard) return fail(CTIS_ERR_INVALID_ARGUMENT, "mlem on a shard plan needs the collective: use ctis_forward + "
-                                                       "all-reduce + ctis_back_update_from_ghat");
+ctis_status run_mlem(ctis_plan_s& P, const float* g, float* f, int64_t frames, int iters, void* ws, cudaStream_t s) {
+  if (P.shard)
+    return fail(CTIS_ERR_INVALID_ARGUMENT,
+                "mlem on a shard plan needs the collective: use ctis_forward + all-reduce + ctis_back_update_from_ghat");
   if (iters < 0) return fail(CTIS_ERR_INVALID_ARGUMENT, "iters < 0");
-  if (frames < 1 || frames > 65535) return fail(CTIS_ERR_INVALID_ARGUMENT, "frames must be in [1, 65535]");
-  ctis_status st = check_ptrs({g, f, ws});
+  ctis_status st = check_frames(frames);
   if (st) return st;
-  DeviceGuard dg(p->device);
-  p->last_launches = 0;
-  if (p->validate) {
-    if ((st = validate_data(p, g, f, frames, s))) return st;
-    p->last_launches += 2;
+  if ((st = check_ptrs({g, f, ws}))) return st;
+  DeviceGuard dg(P.device);
+  P.last_launches = 0;
+  if (P.validate) {
+    if ((st = validate_data(P, g, f, frames, s))) return st;
+    P.last_launches += 2;
   }
   if (iters == 0) return CTIS_OK;
-  float* r = static_cast<float*>(ws);
-  if (!p->use_graph) {
-    CTIS_CUDA(enqueue_iterations(p, g, f, r, (int)frames, iters, s), "mlem launch");
-    p->last_launches += 2LL * iters;
+  float* w = static_cast<float*>(ws);
+  int64_t cnt = 0;
+  if (!P.use_graph) {
+    CTIS_CUDA(enqueue_mlem(P, g, f, w, (int)frames, iters, s, &cnt), "mlem launch");
+    P.last_launches += cnt;
     return CTIS_OK;
   }
   GraphKey key{g, f, ws, frames, iters};
-  auto it = p->graphs.find(key);
-  if (it == p->graphs.end()) {
-    if (p->graphs.size() >= 16) {
-      for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
-      p->graphs.clear();
+  auto it = P.graphs.find(key);
+  if (it == P.graphs.end()) {
+    if (P.graphs.size() >= 16) {
+      for (auto& kv : P.graphs) cudaGraphExecDestroy(kv.second);
+      P.graphs.clear();
     }
     cudaGraph_t graph = nullptr;
-    CTIS_CUDA(cudaStreamBeginCapture(p->side, cudaStreamCaptureModeThreadLocal), "begin capture");
-    cudaError_t e = enqueue_iterations(p, g, f, r, (int)frames, iters, p->side);
-    cudaError_t e2 = cudaStreamEndCapture(p->side, &graph);
-    if (e != cudaSuccess) return cuda_fail(e, "capture launch");
+    CTIS_CUDA(cudaStreamBeginCapture(P.side, cudaStreamCaptureModeThreadLocal), "begin capture");
+    cudaError_t e = enqueue_mlem(P, g, f, w, (int)frames, iters, P.side, &cnt);
+    cudaError_t e2 = cudaStreamEndCapture(P.side, &graph);
+    if (e != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      return cuda_fail(e, "capture launch");
+    }
     if (e2 != cudaSuccess) return cuda_fail(e2, "end capture");
     cudaGraphExec_t exec = nullptr;
     e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
-    it = p->graphs.emplace(key, exec).first;
+    it = P.graphs.emplace(key, exec).first;
+  } else {
+    cnt = (int64_t)iters * ((int64_t)P.fwd.size() + (int64_t)P.back.size() + 1);
   }
-  CTIS_CUDA(cudaEventRecord(p->ev_in, s), "event record");
-  CTIS_CUDA(cudaStreamWaitEvent(p->side, p->ev_in, 0), "stream wait");
-  CTIS_CUDA(cudaGraphLaunch(it->second, p->side), "graph launch");
-  CTIS_CUDA(cudaEventRecord(p->ev_out, p->side), "event record");
-  CTIS_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0), "stream wait");
-  p->last_launches += 2LL * iters;
+  CTIS_CUDA(cudaEventRecord(P.ev_in, s), "event record");
+  CTIS_CUDA(cudaStreamWaitEvent(P.side, P.ev_in, 0), "stream wait");
+  CTIS_CUDA(cudaGraphLaunch(it->second, P.side), "graph launch");
+  CTIS_CUDA(cudaEventRecord(P.ev_out, P.side), "event record");
+  CTIS_CUDA(cudaStreamWaitEvent(s, P.ev_out, 0), "stream wait");
+  P.last_launches += cnt;
   return CTIS_OK;
 }
 
@@ -375,8 +661,7 @@ void ctis_plan_destroy(ctis_plan plan) { delete plan; }
 
 ctis_status ctis_plan_dims(ctis_plan p, int64_t out[10]) {
   if (!p || !out) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL argument");
-  const int64_t v[10] = {p->d.a, p->d.alpha, p->d.w, p->d.gamma, p->d.xi, p->d.n, p->d.m,
-                         p->band_begin, p->band_end, p->total_taps};
+  const int64_t v[10] = {p->a, p->alpha, p->w, p->gamma, p->xi, p->n, p->m, p->band_begin, p->band_end, p->total_taps};
   std::memcpy(out, v, sizeof(v));
   return CTIS_OK;
 }
@@ -393,18 +678,32 @@ ctis_status ctis_set_option(ctis_plan p, int option, int64_t value) {
 
 size_t ctis_workspace_bytes(ctis_plan p, int64_t frames) {
   if (!p || frames < 1) return 0;
-  return (size_t)p->d.n * (size_t)frames * sizeof(float);
+  return 2 * (size_t)p->n * (size_t)frames * sizeof(float);
 }
 
 ctis_status ctis_forward_batched(ctis_plan p, const float* f, float* g_hat, int64_t frames, ctis_stream stream) {
   if (!p) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL plan");
-  if (frames < 1 || frames > 65535) return fail(CTIS_ERR_INVALID_ARGUMENT, "frames must be in [1, 65535]");
-  ctis_status st = check_ptrs({f, g_hat});
+  ctis_status st = check_frames(frames);
   if (st) return st;
+  if ((st = check_ptrs({f, g_hat}))) return st;
   std::lock_guard<std::mutex> lk(p->mu);
   DeviceGuard dg(p->device);
-  CTIS_CUDA(launch_forward(p->d, p->t, f, nullptr, g_hat, (int)frames, false, (cudaStream_t)stream), "forward");
-  p->last_launches = 1;
+  cudaStream_t s = (cudaStream_t)stream;
+  p->last_launches = 0;
+  CTIS_CUDA(cudaMemsetAsync(g_hat, 0, sizeof(float) * (size_t)p->n * frames, s), "forward memset");
+  CTIS_CUDA(enqueue_forward(*p, f, g_hat, (int)frames, s, &p->last_launches), "forward");
+  return CTIS_OK;
+}
+
+ctis_status ctis_forward_accumulate(ctis_plan p, const float* f, float* g_hat, int64_t frames, ctis_stream stream) {
+  if (!p) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL plan");
+  ctis_status st = check_frames(frames);
+  if (st) return st;
+  if ((st = check_ptrs({f, g_hat}))) return st;
+  std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard dg(p->device);
+  p->last_launches = 0;
+  CTIS_CUDA(enqueue_forward(*p, f, g_hat, (int)frames, (cudaStream_t)stream, &p->last_launches), "forward");
   return CTIS_OK;
 }
 
@@ -418,8 +717,8 @@ ctis_status ctis_backproject(ctis_plan p, const float* r, float* z, ctis_stream 
   if (st) return st;
   std::lock_guard<std::mutex> lk(p->mu);
   DeviceGuard dg(p->device);
-  CTIS_CUDA(launch_back(p->d, p->t, r, z, 1, kBackOnly, (cudaStream_t)stream), "backproject");
-  p->last_launches = 1;
+  p->last_launches = 0;
+  CTIS_CUDA(enqueue_back(*p, r, z, 1, 0, (cudaStream_t)stream, &p->last_launches), "backproject");
   return CTIS_OK;
 }
 
@@ -429,22 +728,9 @@ ctis_status ctis_sensitivity(ctis_plan p, float* h, ctis_stream stream) {
   if (st) return st;
   std::lock_guard<std::mutex> lk(p->mu);
   DeviceGuard dg(p->device);
-  CTIS_CUDA(launch_sensitivity(p->d, p->t, h, (cudaStream_t)stream), "sensitivity");
+  CTIS_CUDA(launch_sensitivity(p->d_hband, h, p->ell, p->m, (cudaStream_t)stream), "sensitivity");
   p->last_launches = 1;
   return CTIS_OK;
-}
-
-ctis_status ctis_mlem(ctis_plan p, const float* g, float* f, int iters, void* ws, ctis_stream stream) {
-  if (!p) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL plan");
-  std::lock_guard<std::mutex> lk(p->mu);
-  return run_mlem(p, g, f, 1, iters, ws, (cudaStream_t)stream);
-}
-
-ctis_status ctis_mlem_batched(ctis_plan p, const float* g, float* f, int64_t frames, int iters, void* ws,
-                              ctis_stream stream) {
-  if (!p) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL plan");
-  std::lock_guard<std::mutex> lk(p->mu);
-  return run_mlem(p, g, f, frames, iters, ws, (cudaStream_t)stream);
 }
 
 ctis_status ctis_forward_ratio(ctis_plan p, const float* f, const float* g, float* r, ctis_stream stream) {
@@ -453,8 +739,12 @@ ctis_status ctis_forward_ratio(ctis_plan p, const float* f, const float* g, floa
   if (st) return st;
   std::lock_guard<std::mutex> lk(p->mu);
   DeviceGuard dg(p->device);
-  CTIS_CUDA(launch_forward(p->d, p->t, f, g, r, 1, true, (cudaStream_t)stream), "forward_ratio");
-  p->last_launches = 1;
+  cudaStream_t s = (cudaStream_t)stream;
+  p->last_launches = 0;
+  CTIS_CUDA(cudaMemsetAsync(r, 0, sizeof(float) * (size_t)p->n, s), "forward_ratio memset");
+  CTIS_CUDA(enqueue_forward(*p, f, r, 1, s, &p->last_launches), "forward_ratio forward");
+  CTIS_CUDA(launch_ratio(g, r, r, p->n, false, s), "forward_ratio ratio");
+  p->last_launches += 1;
   return CTIS_OK;
 }
 
@@ -464,9 +754,22 @@ ctis_status ctis_back_update(ctis_plan p, const float* r, float* f, ctis_stream 
   if (st) return st;
   std::lock_guard<std::mutex> lk(p->mu);
   DeviceGuard dg(p->device);
-  CTIS_CUDA(launch_back(p->d, p->t, r, f, 1, kBackUpdate, (cudaStream_t)stream), "back_update");
-  p->last_launches = 1;
+  p->last_launches = 0;
+  CTIS_CUDA(enqueue_back(*p, r, f, 1, 1, (cudaStream_t)stream, &p->last_launches), "back_update");
   return CTIS_OK;
+}
+
+ctis_status ctis_mlem(ctis_plan p, const float* g, float* f, int iters, void* ws, ctis_stream stream) {
+  if (!p) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL plan");
+  std::lock_guard<std::mutex> lk(p->mu);
+  return run_mlem(*p, g, f, 1, iters, ws, (cudaStream_t)stream);
+}
+
+ctis_status ctis_mlem_batched(ctis_plan p, const float* g, float* f, int64_t frames, int iters, void* ws,
+                              ctis_stream stream) {
+  if (!p) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL plan");
+  std::lock_guard<std::mutex> lk(p->mu);
+  return run_mlem(*p, g, f, frames, iters, ws, (cudaStream_t)stream);
 }
 
 ctis_status ctis_back_update_from_ghat(ctis_plan p, const float* g, const float* g_hat, float* f, void* ws,
@@ -476,10 +779,11 @@ ctis_status ctis_back_update_from_ghat(ctis_plan p, const float* g, const float*
   if (st) return st;
   std::lock_guard<std::mutex> lk(p->mu);
   DeviceGuard dg(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
   float* r = static_cast<float*>(ws);
-  CTIS_CUDA(launch_ratio(g, g_hat, r, p->d.n, (cudaStream_t)stream), "ratio");
-  CTIS_CUDA(launch_back(p->d, p->t, r, f, 1, kBackUpdate, (cudaStream_t)stream), "back update");
-  p->last_launches = 2;
+  p->last_launches = 1;
+  CTIS_CUDA(launch_ratio(g, const_cast<float*>(g_hat), r, p->n, false, s), "ratio");
+  CTIS_CUDA(enqueue_back(*p, r, f, 1, 1, s, &p->last_launches), "back update");
   return CTIS_OK;
 }
 
@@ -487,29 +791,28 @@ ctis_status ctis_mlem_host(ctis_plan p, const float* g_host, float* f_host, int6
                            ctis_stream stream) {
   if (!p) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL plan");
   if (!g_host || !f_host) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL host pointer");
-  if (frames < 1 || frames > 65535) return fail(CTIS_ERR_INVALID_ARGUMENT, "frames must be in [1, 65535]");
+  ctis_status st = check_frames(frames);
+  if (st) return st;
   std::lock_guard<std::mutex> lk(p->mu);
   DeviceGuard dg(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   if (p->host_frames < frames) {
-    if (p->d_g) cudaFree(p->d_g);
-    if (p->d_f) cudaFree(p->d_f);
-    if (p->d_ws) cudaFree(p->d_ws);
+    for (void* q : {(void*)p->d_g, (void*)p->d_f, p->d_ws})
+      if (q) cudaFree(q);
     p->d_g = p->d_f = nullptr;
     p->d_ws = nullptr;
     p->host_frames = 0;
     for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
     p->graphs.clear();
-    CTIS_CUDA(cudaMalloc(&p->d_g, sizeof(float) * (size_t)p->d.n * frames), "host-path alloc g");
-    CTIS_CUDA(cudaMalloc(&p->d_f, sizeof(float) * (size_t)p->d.m * frames), "host-path alloc f");
-    CTIS_CUDA(cudaMalloc(&p->d_ws, sizeof(float) * (size_t)p->d.n * frames), "host-path alloc ws");
+    CTIS_CUDA(cudaMalloc(&p->d_g, sizeof(float) * (size_t)p->n * frames), "host-path alloc g");
+    CTIS_CUDA(cudaMalloc(&p->d_f, sizeof(float) * (size_t)p->m * frames), "host-path alloc f");
+    CTIS_CUDA(cudaMalloc(&p->d_ws, 2 * sizeof(float) * (size_t)p->n * frames), "host-path alloc ws");
     p->host_frames = frames;
   }
-  const size_t gb = sizeof(float) * (size_t)p->d.n * frames, fb = sizeof(float) * (size_t)p->d.m * frames;
+  const size_t gb = sizeof(float) * (size_t)p->n * frames, fb = sizeof(float) * (size_t)p->m * frames;
   CTIS_CUDA(cudaMemcpyAsync(p->d_g, g_host, gb, cudaMemcpyHostToDevice, s), "H2D g");
   CTIS_CUDA(cudaMemcpyAsync(p->d_f, f_host, fb, cudaMemcpyHostToDevice, s), "H2D f0");
-  ctis_status st = run_mlem(p, p->d_g, p->d_f, frames, iters, p->d_ws, s);
-  if (st) return st;
+  if ((st = run_mlem(*p, p->d_g, p->d_f, frames, iters, p->d_ws, s))) return st;
   CTIS_CUDA(cudaMemcpyAsync(f_host, p->d_f, fb, cudaMemcpyDeviceToHost, s), "D2H f");
   CTIS_CUDA(cudaStreamSynchronize(s), "host-path sync");
   return CTIS_OK;
@@ -519,6 +822,6 @@ int64_t ctis_last_launch_count(ctis_plan p) { return p ? p->last_launches : 0; }
 
 const char* ctis_last_error(void) { return g_last_error.c_str(); }
 
-const char* ctis_version(void) { return "libctis 0.1.0 (sm_100a)"; }
+const char* ctis_version(void) { return "libctis 0.2.0 (sm_100a, per-plan __constant__ tap pages)"; }
 
 }  // extern "C"

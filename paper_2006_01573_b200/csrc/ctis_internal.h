@@ -1,70 +1,58 @@
-// Internal declarations shared by the plan builder (ctis_api.cu) and the kernels
+// Internal declarations shared by the plan builder (ctis_api.cu), the per-plan
+// table kernels (ctis_tables.cu -> embedded cubin) and the element-wise kernels
 // (ctis_kernels.cu).  Not part of the public ABI (include/ctis.h is).
 #pragma once
 
-#include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace ctis {
 
 // ---------------------------------------------------------------------------
-// Forward projection tiles (output-stationary gather over the FPA).
-// A tap (o, w) of band lam is a 1-D cyclic shift by o on the column-major
-// flattened FPA (Eq. 7).  On the 2-D FPA that shift is, for
-// each voxel (r, c), either (r+dr, c+dc), (r+dr-gamma, c+dc+1) [carry into the
-// next column] and, modulo xi, a wrap past the last column.  So every tap is
-// exactly <= 4 rectangle "pieces" of the field stop, each a pure 2-D
-// translation.  The builder clips each piece against the forward tiles and
-// stores one FwdEntry per (tile, piece):
-//   FPA pixel (R, C) of the clip rectangle receives w * f[base + R + a*C].
-constexpr int kFwdTileR = 64;   // FPA rows per forward tile (gamma direction, contiguous)
-constexpr int kFwdTileC = 16;   // FPA columns per forward tile
-constexpr int kFwdThreads = 256;
+// Tap tables live in __constant__ memory ("pages" of 64 KB).  Every plan loads
+// its own instance of the table-kernel cubin per page (cudaLibraryLoadData), so
+// each page is private to the plan.  Kernels read taps through the uniform
+// datapath (LDCU -> FFMA R, R, UR, R): tap metadata costs no L1/SMEM bandwidth.
+constexpr int kPageWords = 16384;  // 64 KB of uint32
 
-struct FwdEntry {
-  int base;            // lam*l - sr - a*sc, so that f index = base + R + a*C
-  float w;             // tap weight
-  int R0, R1, C0, C1;  // clip rectangle on the FPA, half-open, inside the tile
-  int full;            // rectangle covers the whole tile: no per-pixel test
-  int pad;
+// Page layout (uint32 words):
+//   [0]       number of chunks in the page
+//   [1 + k]   word offset of chunk k's descriptor
+//
+// Forward chunk descriptor (Eq. 12 evaluated per "mode"):
+//   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] u_r0   [D+4] u_c0   [D+5] tiles_r   [D+6] tiles_c  [D+7] 0
+//   [D+8 ..]            o_ref[c]                     (nm words, 1-D reference offset in [0, n))
+//   [BI = D+8+nm ..]    per band b: row0_rel, col0_rel, WR, WC   (window rows/cols relative to the tile)
+//   [TP = BI+4*nb ..]   per (b, c): off, w-bits     (index TP + 2*(b*nm + c); w = 0 -> no tap)
+// Back chunk descriptor (Eqs. 14-15):
+//   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] tiles_r   [D+4] tiles_c   [D+5..7] 0
+//   [MI = D+8 ..]       per mode c: Bm, WR, WC, 0    (window origin term in [0, n))
+//   [TP = MI+4*nm ..]   per (c, b): off, w-bits     (index TP + 2*(c*nb + b))
+//   [IH = TP+2*nm*nb..] inv_h[b]
+enum : int { kDescHeader = 8 };
+
+// Forward kernel geometry: one u-space position per thread, 32 rows x 16 columns per CTA.
+constexpr int kFwdTR = 32;
+constexpr int kFwdTC = 16;
+constexpr int kFwdThreads = kFwdTR * kFwdTC;
+constexpr int kFwdBands = 16;           // bands per forward chunk
+// Back kernel geometry: 32 x 32 voxel tile, 2 voxels per thread, kBackBands bands.
+constexpr int kBackTR = 32;
+constexpr int kBackTC = 32;
+constexpr int kBackThreads = 512;
+constexpr int kBackBands = 16;
+
+// Shared-memory window capacity (floats per buffer, two buffers per CTA).
+constexpr int kFwdWinFloats = 5120;     // 20 KB
+constexpr int kBackWinFloats = 5120;
+
+// Per-launch parameters of the table kernels.
+struct TabArgs {
+  const float* src;    // forward: f; back: r
+  float* dst;          // forward: g_hat (accumulated with red.add); back: f (updated) or z
+  long long src_frame; // elements between frames in src
+  long long dst_frame; // elements between frames in dst
+  int a, alpha, gamma, n, ell;
+  int mode;            // back: 1 = update f in place, 0 = write z
 };
-static_assert(sizeof(FwdEntry) == 32, "FwdEntry must stay 32 bytes");
-
-// ---------------------------------------------------------------------------
-// Back projection (voxel-stationary gather from r).
-// z_lam[r, c] = sum_t w_t * r[(r + gamma*c + o_t) mod n]   (Eqs. 14-15)
-constexpr int kBackTileR = 32;  // voxel rows per CTA (one warp lane each)
-constexpr int kBackTileC = 8;   // voxel columns per CTA (one warp each)
-constexpr int kBackBands = 4;   // bands per CTA
-constexpr int kBackThreads = kBackTileR * kBackTileC;
-
-struct DevTables {
-  // forward
-  const FwdEntry* fwd_entries;
-  const int* fwd_tile_ptr;     // tiles+1
-  int tiles_r, tiles_c;
-  // back: taps per band, offsets/weights padded to a multiple of 4 per band
-  const int* band_ptr4;        // w+1, start of band lam in the padded arrays (multiple of 4)
-  const int* band_cnt;         // w, real tap count of band lam
-  const int* tap_off;          // padded, int32 offsets in [0, n)
-  const float* tap_w;          // padded
-  const float* inv_h;          // w, 1/h_lam (float32)
-  const float* h;              // w, h_lam (float32)
-};
-
-struct Dims {
-  int a, alpha, w, gamma, xi;
-  int n, ell, m;
-};
-
-// Kernel launchers (ctis_kernels.cu).  All return the cudaGetLastError() of the launch.
-cudaError_t launch_forward(const Dims& d, const DevTables& t, const float* f, const float* g,
-                           float* out, int frames, bool ratio, cudaStream_t s);
-enum BackMode { kBackOnly = 0, kBackUpdate = 1 };
-cudaError_t launch_back(const Dims& d, const DevTables& t, const float* r, float* fz, int frames,
-                        BackMode mode, cudaStream_t s);
-cudaError_t launch_sensitivity(const Dims& d, const DevTables& t, float* h, cudaStream_t s);
-cudaError_t launch_ratio(const float* g, const float* ghat, float* r, int64_t count, cudaStream_t s);
-cudaError_t launch_validate(const float* x, int64_t count, int* flag, cudaStream_t s);
 
 }  // namespace ctis

@@ -1,0 +1,252 @@
+// ctis_tables.cu — the two projection kernels of the CTIS MLEM hot path, compiled to a
+// standalone sm_100a cubin that libctis embeds and loads once per plan and tap page
+// (cudaLibraryLoadData), so that every plan owns private __constant__ tap tables.
+//
+//   forward  g_hat = H f = sum_lam C_lam E f_lam        (Eqs. 8-13; Alg. 1 l. 6-7)
+//   back     z = H^T r,  f <- f (.) z (/) h              (Eqs. 14-17; Eq. 2; l. 9-12)
+//
+// Both evaluate the circulant products directly from the sparse first columns c_lam
+// ("taps"): voxel q of band lam meets FPA pixel (E(q) + o) mod n with weight w
+// for every tap (o, w) of c_lam.  Writing o = o_ref + dr + gamma*dc for a per-chunk
+// "mode" reference o_ref (taps of consecutive bands that drift together, e.g. one
+// diffraction order) turns each tap into a small 2-D shift (dr, dc) of the field stop:
+//   E(q) + o = E(q + (dr, dc)) + o_ref   (exact integer identity, so the 1-D cyclic
+//   wrap of Eq. 7 is reproduced exactly by reducing the final index mod n).
+//
+// forward ("constellation"): a CTA owns a 32 x 16 tile of u = q + (dr, dc) space and ALL
+//   modes of a chunk of bands.  Per band it stages one shared-memory window of f_lam
+//   (cp.async, zero outside the field stop) that every mode reads, accumulates
+//   acc[mode] += w * f_lam[u - (dr, dc)] in registers, and finally adds acc[mode] to
+//   g_hat[(E(u) + o_ref) mod n] with red.global.add.f32 (chunks of bands overlap there).
+// back: a CTA owns a 32 x 32 voxel tile and a chunk of 16 bands; per mode it stages one
+//   shared-memory window of r (1-D modular addressing, exact wrap) that every band of the
+//   chunk reads, accumulates z[band] for 2 voxels per thread in registers, and fuses the
+//   multiplicative update f <- f * z * (1/h_lam) into the epilogue.
+// Tap metadata (window offsets, weights) is read from __constant__ through the uniform
+// datapath (LDCU + FFMA R,R,UR,R): the only per-FMA shared-memory traffic is the operand.
+#include <stdint.h>
+
+#include "ctis_internal.h"
+
+using namespace ctis;
+
+__constant__ uint32_t c_tab[kPageWords];
+
+namespace {
+
+__device__ __forceinline__ void cp_async16(float* smem, const float* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+}
+
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+}
+
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ int tabi(uint32_t i) { return (int)c_tab[i]; }
+__device__ __forceinline__ float tabf(uint32_t i) { return __uint_as_float(c_tab[i]); }
+
+// f_lam window: element (i, j) = f_lam[(row0 + i) + a*(col0 + j)], zero outside the field stop.
+template <bool VEC>
+__device__ __forceinline__ void load_f_window(float* buf, const float* fl, const TabArgs& A, int row0, int col0,
+                                              int WR, int WC) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kFwdThreads / 32;
+  for (int j = warp; j < WC; j += NW) {
+    const int cc = col0 + j;
+    const bool cok = (cc >= 0) & (cc < A.alpha);
+    const float* col = fl + (long long)A.a * cc;
+    if (VEC) {
+      for (int i = lane * 4; i < WR; i += 128) {
+        const int rr = row0 + i;
+        const bool ok = cok & (rr >= 0) & (rr < A.a);
+        cp_async16(buf + i + WR * j, ok ? col + rr : fl, ok);
+      }
+    } else {
+      for (int i = lane; i < WR; i += 32) {
+        const int rr = row0 + i;
+        const bool ok = cok & (rr >= 0) & (rr < A.a);
+        cp_async4(buf + i + WR * j, ok ? col + rr : fl, ok);
+      }
+    }
+  }
+}
+
+// r window: element (i, j) = r[(B + i + gamma*j) mod n]  (B in [0, n)).
+template <bool VEC>
+__device__ __forceinline__ void load_r_window(float* buf, const float* r, const TabArgs& A, long long B, int WR,
+                                              int WC) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kBackThreads / 32;
+  for (int j = warp; j < WC; j += NW) {
+    long long cb = B + (long long)A.gamma * j;
+    if (cb >= A.n) cb %= A.n;
+    if (VEC) {
+      for (int i = lane * 4; i < WR; i += 128) {
+        long long idx = cb + i;
+        if (idx >= A.n) idx %= A.n;
+        cp_async16(buf + i + WR * j, r + idx, true);
+      }
+    } else {
+      for (int i = lane; i < WR; i += 32) {
+        long long idx = cb + i;
+        if (idx >= A.n) idx %= A.n;
+        cp_async4(buf + i + WR * j, r + idx, true);
+      }
+    }
+  }
+}
+
+template <int MAXM, bool VEC>
+__device__ __forceinline__ void forward_body(const TabArgs& A) {
+  extern __shared__ __align__(16) float smem[];
+  const uint32_t D = c_tab[1 + blockIdx.y];
+  const int lam0 = tabi(D + 0), nb = tabi(D + 1), nm = tabi(D + 2);
+  const int u_r0 = tabi(D + 3), u_c0 = tabi(D + 4), tiles_r = tabi(D + 5), tiles_c = tabi(D + 6);
+  const int tile = blockIdx.x;
+  if (tile >= tiles_r * tiles_c) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int U_r = u_r0 + (tile % tiles_r) * kFwdTR, U_c = u_c0 + (tile / tiles_r) * kFwdTC;
+  const float* f = A.src + (long long)blockIdx.z * A.src_frame;
+  const uint32_t BI = D + kDescHeader + nm, TP = BI + 4 * nb;
+
+  float acc[MAXM];
+#pragma unroll
+  for (int c = 0; c < MAXM; ++c) acc[c] = 0.f;
+
+  load_f_window<VEC>(smem, f + (long long)lam0 * A.ell, A, U_r + tabi(BI + 0), U_c + tabi(BI + 1), tabi(BI + 2),
+                     tabi(BI + 3));
+  cp_commit();
+  for (int b = 0; b < nb; ++b) {
+    if (b + 1 < nb) {
+      const uint32_t bi = BI + 4 * (b + 1);
+      load_f_window<VEC>(smem + ((b + 1) & 1) * kFwdWinFloats, f + (long long)(lam0 + b + 1) * A.ell, A,
+                         U_r + tabi(bi + 0), U_c + tabi(bi + 1), tabi(bi + 2), tabi(bi + 3));
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const float* win = smem + (b & 1) * kFwdWinFloats;
+    const int base = lane + tabi(BI + 4 * b + 2) * warp;
+    const uint32_t tp = TP + 2 * b * nm;
+#pragma unroll
+    for (int c = 0; c < MAXM; ++c) {
+      if (c < nm) {
+        const float w = tabf(tp + 2 * c + 1);
+        if (w != 0.f) acc[c] = fmaf(w, win[base + tabi(tp + 2 * c)], acc[c]);
+      }
+    }
+    __syncthreads();
+  }
+  float* g = A.dst + (long long)blockIdx.z * A.dst_frame;
+  const long long ub = (long long)(U_r + lane) + (long long)A.gamma * (U_c + warp);
+#pragma unroll
+  for (int c = 0; c < MAXM; ++c) {
+    if (c < nm && acc[c] != 0.f) {
+      long long P = (ub + tabi(D + kDescHeader + c)) % A.n;
+      if (P < 0) P += A.n;
+      atomicAdd(g + P, acc[c]);
+    }
+  }
+}
+
+template <bool VEC>
+__device__ __forceinline__ void back_body(const TabArgs& A) {
+  extern __shared__ __align__(16) float smem[];
+  const uint32_t D = c_tab[1 + blockIdx.y];
+  const int lam0 = tabi(D + 0), nb = tabi(D + 1), nm = tabi(D + 2);
+  const int tiles_r = tabi(D + 3), tiles_c = tabi(D + 4);
+  const int tile = blockIdx.x;
+  if (tile >= tiles_r * tiles_c) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q_r0 = (tile % tiles_r) * kBackTR, q_c0 = (tile / tiles_r) * kBackTC;
+  const float* r = A.src + (long long)blockIdx.z * A.src_frame;
+  const uint32_t MI = D + kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * nb;
+  const long long tile1d = (long long)q_r0 + (long long)A.gamma * q_c0;
+
+  float acc0[kBackBands], acc1[kBackBands];
+#pragma unroll
+  for (int b = 0; b < kBackBands; ++b) acc0[b] = acc1[b] = 0.f;
+
+  auto origin = [&](int c) {
+    long long B = tile1d + tabi(MI + 4 * c);
+    if (B >= A.n) B %= A.n;
+    return B;
+  };
+  load_r_window<VEC>(smem, r, A, origin(0), tabi(MI + 1), tabi(MI + 2));
+  cp_commit();
+  for (int c = 0; c < nm; ++c) {
+    if (c + 1 < nm) {
+      load_r_window<VEC>(smem + ((c + 1) & 1) * kBackWinFloats, r, A, origin(c + 1), tabi(MI + 4 * (c + 1) + 1),
+                         tabi(MI + 4 * (c + 1) + 2));
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const float* win = smem + (c & 1) * kBackWinFloats;
+    const int WR = tabi(MI + 4 * c + 1);
+    const float* w0 = win + lane + WR * warp;
+    const float* w1 = w0 + WR * (kBackThreads / 32);
+    const uint32_t tp = TP + 2 * c * nb;
+#pragma unroll
+    for (int b = 0; b < kBackBands; ++b) {
+      if (b < nb) {
+        const float w = tabf(tp + 2 * b + 1);
+        if (w != 0.f) {
+          const int off = tabi(tp + 2 * b);
+          acc0[b] = fmaf(w, w0[off], acc0[b]);
+          acc1[b] = fmaf(w, w1[off], acc1[b]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  float* f = A.dst + (long long)blockIdx.z * A.dst_frame;
+  const int qr = q_r0 + lane, qc0 = q_c0 + warp, qc1 = qc0 + kBackThreads / 32;
+  if (qr >= A.a) return;
+#pragma unroll
+  for (int b = 0; b < kBackBands; ++b) {
+    if (b < nb) {
+      const long long lb = (long long)(lam0 + b) * A.ell + qr;
+      const float ih = tabf(IH + b);
+      if (qc0 < A.alpha) {
+        float* p = f + lb + (long long)A.a * qc0;
+        *p = A.mode ? (*p) * acc0[b] * ih : acc0[b];
+      }
+      if (qc1 < A.alpha) {
+        float* p = f + lb + (long long)A.a * qc1;
+        *p = A.mode ? (*p) * acc1[b] * ih : acc1[b];
+      }
+    }
+  }
+}
+
+}  // namespace
+
+#define CTIS_FWD(M, V, NAME) \
+  extern "C" __global__ void __launch_bounds__(kFwdThreads, 1) NAME(const TabArgs A) { forward_body<M, V>(A); }
+CTIS_FWD(16, true, ctis_fwd_m16_v)
+CTIS_FWD(32, true, ctis_fwd_m32_v)
+CTIS_FWD(64, true, ctis_fwd_m64_v)
+CTIS_FWD(96, true, ctis_fwd_m96_v)
+CTIS_FWD(16, false, ctis_fwd_m16_s)
+CTIS_FWD(32, false, ctis_fwd_m32_s)
+CTIS_FWD(64, false, ctis_fwd_m64_s)
+CTIS_FWD(96, false, ctis_fwd_m96_s)
+
+extern "C" __global__ void __launch_bounds__(kBackThreads, 2) ctis_back_v(const TabArgs A) { back_body<true>(A); }
+extern "C" __global__ void __launch_bounds__(kBackThreads, 2) ctis_back_s(const TabArgs A) { back_body<false>(A); }
