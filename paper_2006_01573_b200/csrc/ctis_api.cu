@@ -200,7 +200,7 @@ inline uint32_t fbits(float x) {
 }
 
 // Forward chunk descriptor for bands [b0, b0+nb) (local) and the given modes.
-bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const Mode*>& ms, bool vec,
+bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const Mode*>& ms, int maxm, bool vec,
                   std::vector<uint32_t>& out, int& tiles) {
   const int nm = (int)ms.size();
   std::vector<int> rmin(nb, INT_MAX), rmax(nb, INT_MIN), cmin(nb, INT_MAX), cmax(nb, INT_MIN);
@@ -221,7 +221,7 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
   const int u_r0 = Rmin, u_c0 = Cmin;
   const int tiles_r = (P.a + Rmax - Rmin + kFwdTR - 1) / kFwdTR;
   const int tiles_c = (P.alpha + Cmax - Cmin + kFwdTC - 1) / kFwdTC;
-  out.assign(kDescHeader + nm + 4 * nb + 2 * nb * nm, 0u);
+  out.assign(kDescHeader + nm + 4 * nb + 2 * nb * maxm, 0u);
   out[0] = (uint32_t)b0;
   out[1] = (uint32_t)nb;
   out[2] = (uint32_t)nm;
@@ -229,6 +229,7 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
   out[4] = (uint32_t)u_c0;
   out[5] = (uint32_t)tiles_r;
   out[6] = (uint32_t)tiles_c;
+  out[7] = (uint32_t)maxm;
   for (int c = 0; c < nm; ++c) out[kDescHeader + c] = (uint32_t)(ms[c]->ref_dr + P.gamma * ms[c]->ref_dc);
   const int BI = kDescHeader + nm, TP = BI + 4 * nb;
   std::vector<int> WRs(nb, 4), lead(nb, 0);
@@ -253,8 +254,8 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
     for (const ModeTap& t : ms[c]->taps) {
       const int dr = t.dr - ms[c]->ref_dr, dc = t.dc - ms[c]->ref_dc;
       const int off = (rmax[t.b] + lead[t.b] - dr) + WRs[t.b] * (cmax[t.b] - dc);
-      out[TP + 2 * (t.b * nm + c)] = (uint32_t)off;
-      out[TP + 2 * (t.b * nm + c) + 1] = fbits(t.w);
+      out[TP + 2 * (t.b * maxm + c)] = (uint32_t)(4 * off);
+      out[TP + 2 * (t.b * maxm + c) + 1] = fbits(t.w);
     }
   tiles = tiles_r * tiles_c;
   return true;
@@ -264,14 +265,14 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
 bool back_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<Mode>& ms, const std::vector<float>& invh,
                bool vec, std::vector<uint32_t>& out, int& tiles) {
   const int nm = (int)ms.size();
-  out.assign(kDescHeader + 4 * nm + 2 * nm * nb + nb, 0u);
+  out.assign(kDescHeader + 4 * nm + 2 * nm * kBackBands + nb, 0u);
   const int tiles_r = (P.a + kBackTR - 1) / kBackTR, tiles_c = (P.alpha + kBackTC - 1) / kBackTC;
   out[0] = (uint32_t)b0;
   out[1] = (uint32_t)nb;
   out[2] = (uint32_t)nm;
   out[3] = (uint32_t)tiles_r;
   out[4] = (uint32_t)tiles_c;
-  const int MI = kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * nb;
+  const int MI = kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * kBackBands;
   for (int c = 0; c < nm; ++c) {
     const Mode& md = ms[c];
     int rmin = INT_MAX, rmax = INT_MIN, cmin = INT_MAX, cmax = INT_MIN;
@@ -295,8 +296,8 @@ bool back_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<Mode>& ms
     out[MI + 4 * c + 2] = (uint32_t)WC;
     for (const ModeTap& t : md.taps) {
       const int dr = t.dr - md.ref_dr, dc = t.dc - md.ref_dc;
-      out[TP + 2 * (c * nb + t.b)] = (uint32_t)((dr - rmin + lead) + WR * (dc - cmin));
-      out[TP + 2 * (c * nb + t.b) + 1] = fbits(t.w);
+      out[TP + 2 * (c * kBackBands + t.b)] = (uint32_t)(4 * ((dr - rmin + lead) + WR * (dc - cmin)));
+      out[TP + 2 * (c * kBackBands + t.b) + 1] = fbits(t.w);
     }
   }
   for (int b = 0; b < nb; ++b) out[IH + b] = fbits(invh[b0 + b]);
@@ -352,8 +353,7 @@ ctis_status load_page(Page& pg, bool vec) {
   CTIS_CUDA(cudaMemcpy(dptr, pg.words.data(), pg.words.size() * 4, cudaMemcpyHostToDevice), "upload tap page");
   std::string name;
   if (pg.forward) {
-    const int mm = pg.max_modes <= 16 ? 16 : pg.max_modes <= 32 ? 32 : pg.max_modes <= 64 ? 64 : 96;
-    name = "ctis_fwd_m" + std::to_string(mm) + (vec ? "_v" : "_s");
+    name = "ctis_fwd_m" + std::to_string(pg.max_modes) + (vec ? "_v" : "_s");
   } else {
     name = std::string("ctis_back") + (vec ? "_v" : "_s");
   }
@@ -364,24 +364,32 @@ ctis_status load_page(Page& pg, bool vec) {
 ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& bands, const std::vector<float>& invh) {
   P.vec_f = (P.a % 4 == 0);
   P.vec_b = (P.gamma % 4 == 0);
-  // ---- forward: chunks of kFwdBands bands, modes split into passes of <= 96
+  // ---- forward: chunks of kFwdBands bands, modes split into passes of <= 96; one MAXM (nm rounded
+  //      up to 8) for the whole plan so that every forward page runs the same kernel template
   {
-    std::vector<std::vector<uint32_t>> descs;
-    std::vector<int> tiles, modes;
+    std::vector<std::vector<Mode>> chunk_modes;
+    int maxm = 8;
     for (int b0 = 0; b0 < P.w; b0 += kFwdBands) {
       const int nb = std::min(kFwdBands, P.w - b0);
       std::vector<std::vector<TapXY>> cb(bands.begin() + b0, bands.begin() + b0 + nb);
-      std::vector<Mode> ms = cluster_modes(cb);
-      for (size_t s = 0; s < ms.size(); s += 96) {
+      chunk_modes.push_back(cluster_modes(cb));
+      maxm = std::max(maxm, std::min(96, ((int)chunk_modes.back().size() + 7) / 8 * 8));
+    }
+    std::vector<std::vector<uint32_t>> descs;
+    std::vector<int> tiles, modes;
+    for (size_t k = 0; k < chunk_modes.size(); ++k) {
+      const int b0 = (int)k * kFwdBands, nb = std::min(kFwdBands, P.w - b0);
+      const std::vector<Mode>& ms = chunk_modes[k];
+      for (size_t s0 = 0; s0 < ms.size(); s0 += (size_t)maxm) {
         std::vector<const Mode*> pass;
-        for (size_t c = s; c < std::min(ms.size(), s + 96); ++c) pass.push_back(&ms[c]);
+        for (size_t c = s0; c < std::min(ms.size(), s0 + (size_t)maxm); ++c) pass.push_back(&ms[c]);
         std::vector<uint32_t> d;
         int t = 0;
-        if (!forward_desc(P, b0, nb, pass, P.vec_f, d, t)) return fail(CTIS_ERR_TAP, "forward window overflow");
+        if (!forward_desc(P, b0, nb, pass, maxm, P.vec_f, d, t)) return fail(CTIS_ERR_TAP, "forward window overflow");
         if (d.empty()) continue;
         descs.push_back(std::move(d));
         tiles.push_back(t);
-        modes.push_back((int)pass.size());
+        modes.push_back(maxm);
       }
     }
     pack_pages(P.fwd, true, descs, tiles, modes);
@@ -573,7 +581,7 @@ ctis_status validate_data(ctis_plan_s& P, const float* g, const float* f, int64_
 cudaError_t enqueue_mlem(ctis_plan_s& P, const float* g, float* f, float* ws, int frames, int iters, cudaStream_t s,
                          int64_t* cnt) {
   float* A = ws;
-  float* B = ws + (size_t)P.n * frames;
+  float* B = ws + (((size_t)P.n * frames + 3) & ~(size_t)3);  // 16-byte aligned second half
   const long long count = (long long)P.n * frames;
   cudaError_t e = cudaMemsetAsync(A, 0, sizeof(float) * (size_t)count, s);
   for (int k = 0; k < iters && e == cudaSuccess; ++k) {
@@ -678,7 +686,7 @@ ctis_status ctis_set_option(ctis_plan p, int option, int64_t value) {
 
 size_t ctis_workspace_bytes(ctis_plan p, int64_t frames) {
   if (!p || frames < 1) return 0;
-  return 2 * (size_t)p->n * (size_t)frames * sizeof(float);
+  return 2 * (((size_t)p->n * (size_t)frames + 3) & ~(size_t)3) * sizeof(float);
 }
 
 ctis_status ctis_forward_batched(ctis_plan p, const float* f, float* g_hat, int64_t frames, ctis_stream stream) {
@@ -806,7 +814,7 @@ ctis_status ctis_mlem_host(ctis_plan p, const float* g_host, float* f_host, int6
     p->graphs.clear();
     CTIS_CUDA(cudaMalloc(&p->d_g, sizeof(float) * (size_t)p->n * frames), "host-path alloc g");
     CTIS_CUDA(cudaMalloc(&p->d_f, sizeof(float) * (size_t)p->m * frames), "host-path alloc f");
-    CTIS_CUDA(cudaMalloc(&p->d_ws, 2 * sizeof(float) * (size_t)p->n * frames), "host-path alloc ws");
+    CTIS_CUDA(cudaMalloc(&p->d_ws, ctis_workspace_bytes(p, frames)), "host-path alloc ws");
     p->host_frames = frames;
   }
   const size_t gb = sizeof(float) * (size_t)p->n * frames, fb = sizeof(float) * (size_t)p->m * frames;

@@ -19,15 +19,16 @@ constexpr int kPageWords = 16384;  // 64 KB of uint32
 //   [1 + k]   word offset of chunk k's descriptor
 //
 // Forward chunk descriptor (Eq. 12 evaluated per "mode"):
-//   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] u_r0   [D+4] u_c0   [D+5] tiles_r   [D+6] tiles_c  [D+7] 0
+//   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] u_r0   [D+4] u_c0   [D+5] tiles_r   [D+6] tiles_c  [D+7] MAXM
 //   [D+8 ..]            o_ref[c]                     (nm words, 1-D reference offset in [0, n))
 //   [BI = D+8+nm ..]    per band b: row0_rel, col0_rel, WR, WC   (window rows/cols relative to the tile)
-//   [TP = BI+4*nb ..]   per (b, c): off, w-bits     (index TP + 2*(b*nm + c); w = 0 -> no tap)
+//   [TP = BI+4*nb ..]   per (b, c), c < MAXM: byte offset, w-bits  (index TP + 2*(b*MAXM + c);
+//                       w = 0 -> no tap; MAXM = nm rounded up to 8 = the kernel template)
 // Back chunk descriptor (Eqs. 14-15):
 //   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] tiles_r   [D+4] tiles_c   [D+5..7] 0
 //   [MI = D+8 ..]       per mode c: Bm, WR, WC, 0    (window origin term in [0, n))
-//   [TP = MI+4*nm ..]   per (c, b): off, w-bits     (index TP + 2*(c*nb + b))
-//   [IH = TP+2*nm*nb..] inv_h[b]
+//   [TP = MI+4*nm ..]   per (c, b), b < kBackBands: byte offset, w-bits  (index TP + 2*(c*kBackBands + b))
+//   [IH = TP+2*nm*kBackBands ..] inv_h[b]
 enum : int { kDescHeader = 8 };
 
 // Forward kernel geometry: one u-space position per thread, 32 rows x 16 columns per CTA.

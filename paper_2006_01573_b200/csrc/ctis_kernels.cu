@@ -4,6 +4,7 @@
 //   validate  flag data that EM cannot take (negative, NaN, Inf)
 // The projections themselves live in ctis_tables.cu (per-plan cubin with __constant__ taps).
 #include <cuda_runtime.h>
+#include <stdint.h>
 
 #include "ctis_kernels.h"
 
@@ -13,7 +14,9 @@ namespace ctis {
 // forward projection can accumulate into it with red.add).  Vectorised by 4 when aligned.
 __global__ void ratio_kernel(const float* __restrict__ g, float* gh, float* r,
                              long long count, int zero_ghat) {
-  const long long n4 = count >> 2;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(gh) |
+                         reinterpret_cast<uintptr_t>(r)) & 15u) == 0;
+  const long long n4 = aligned ? (count >> 2) : 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   for (long long i = t0; i < n4; i += stride) {

@@ -107,6 +107,12 @@ __device__ __forceinline__ void load_r_window(float* buf, const float* r, const 
   }
 }
 
+__device__ __forceinline__ float lds(unsigned addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
 template <int MAXM, bool VEC>
 __device__ __forceinline__ void forward_body(const TabArgs& A) {
   extern __shared__ __align__(16) float smem[];
@@ -119,6 +125,7 @@ __device__ __forceinline__ void forward_body(const TabArgs& A) {
   const int U_r = u_r0 + (tile % tiles_r) * kFwdTR, U_c = u_c0 + (tile / tiles_r) * kFwdTC;
   const float* f = A.src + (long long)blockIdx.z * A.src_frame;
   const uint32_t BI = D + kDescHeader + nm, TP = BI + 4 * nb;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
 
   float acc[MAXM];
 #pragma unroll
@@ -138,16 +145,11 @@ __device__ __forceinline__ void forward_body(const TabArgs& A) {
       cp_wait<0>();
     }
     __syncthreads();
-    const float* win = smem + (b & 1) * kFwdWinFloats;
-    const int base = lane + tabi(BI + 4 * b + 2) * warp;
-    const uint32_t tp = TP + 2 * b * nm;
+    // byte address of this thread's u in the window; tap entries hold byte offsets (absent: w = 0)
+    const unsigned base = sbase + 4u * ((b & 1) * kFwdWinFloats + lane + tabi(BI + 4 * b + 2) * warp);
+    const uint32_t tp = TP + 2 * b * MAXM;
 #pragma unroll
-    for (int c = 0; c < MAXM; ++c) {
-      if (c < nm) {
-        const float w = tabf(tp + 2 * c + 1);
-        if (w != 0.f) acc[c] = fmaf(w, win[base + tabi(tp + 2 * c)], acc[c]);
-      }
-    }
+    for (int c = 0; c < MAXM; ++c) acc[c] = fmaf(tabf(tp + 2 * c + 1), lds(base + c_tab[tp + 2 * c]), acc[c]);
     __syncthreads();
   }
   float* g = A.dst + (long long)blockIdx.z * A.dst_frame;
@@ -173,7 +175,8 @@ __device__ __forceinline__ void back_body(const TabArgs& A) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q_r0 = (tile % tiles_r) * kBackTR, q_c0 = (tile / tiles_r) * kBackTC;
   const float* r = A.src + (long long)blockIdx.z * A.src_frame;
-  const uint32_t MI = D + kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * nb;
+  const uint32_t MI = D + kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * kBackBands;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
   const long long tile1d = (long long)q_r0 + (long long)A.gamma * q_c0;
 
   float acc0[kBackBands], acc1[kBackBands];
@@ -197,21 +200,16 @@ __device__ __forceinline__ void back_body(const TabArgs& A) {
       cp_wait<0>();
     }
     __syncthreads();
-    const float* win = smem + (c & 1) * kBackWinFloats;
     const int WR = tabi(MI + 4 * c + 1);
-    const float* w0 = win + lane + WR * warp;
-    const float* w1 = w0 + WR * (kBackThreads / 32);
-    const uint32_t tp = TP + 2 * c * nb;
+    const unsigned b0a = sbase + 4u * ((c & 1) * kBackWinFloats + lane + WR * warp);
+    const unsigned b1a = b0a + 4u * WR * (kBackThreads / 32);
+    const uint32_t tp = TP + 2 * c * kBackBands;
 #pragma unroll
     for (int b = 0; b < kBackBands; ++b) {
-      if (b < nb) {
-        const float w = tabf(tp + 2 * b + 1);
-        if (w != 0.f) {
-          const int off = tabi(tp + 2 * b);
-          acc0[b] = fmaf(w, w0[off], acc0[b]);
-          acc1[b] = fmaf(w, w1[off], acc1[b]);
-        }
-      }
+      const float w = tabf(tp + 2 * b + 1);
+      const unsigned off = c_tab[tp + 2 * b];
+      acc0[b] = fmaf(w, lds(b0a + off), acc0[b]);
+      acc1[b] = fmaf(w, lds(b1a + off), acc1[b]);
     }
     __syncthreads();
   }
@@ -239,13 +237,29 @@ __device__ __forceinline__ void back_body(const TabArgs& A) {
 
 #define CTIS_FWD(M, V, NAME) \
   extern "C" __global__ void __launch_bounds__(kFwdThreads, 1) NAME(const TabArgs A) { forward_body<M, V>(A); }
+CTIS_FWD(8, true, ctis_fwd_m8_v)
+CTIS_FWD(8, false, ctis_fwd_m8_s)
 CTIS_FWD(16, true, ctis_fwd_m16_v)
-CTIS_FWD(32, true, ctis_fwd_m32_v)
-CTIS_FWD(64, true, ctis_fwd_m64_v)
-CTIS_FWD(96, true, ctis_fwd_m96_v)
 CTIS_FWD(16, false, ctis_fwd_m16_s)
+CTIS_FWD(24, true, ctis_fwd_m24_v)
+CTIS_FWD(24, false, ctis_fwd_m24_s)
+CTIS_FWD(32, true, ctis_fwd_m32_v)
 CTIS_FWD(32, false, ctis_fwd_m32_s)
+CTIS_FWD(40, true, ctis_fwd_m40_v)
+CTIS_FWD(40, false, ctis_fwd_m40_s)
+CTIS_FWD(48, true, ctis_fwd_m48_v)
+CTIS_FWD(48, false, ctis_fwd_m48_s)
+CTIS_FWD(56, true, ctis_fwd_m56_v)
+CTIS_FWD(56, false, ctis_fwd_m56_s)
+CTIS_FWD(64, true, ctis_fwd_m64_v)
 CTIS_FWD(64, false, ctis_fwd_m64_s)
+CTIS_FWD(72, true, ctis_fwd_m72_v)
+CTIS_FWD(72, false, ctis_fwd_m72_s)
+CTIS_FWD(80, true, ctis_fwd_m80_v)
+CTIS_FWD(80, false, ctis_fwd_m80_s)
+CTIS_FWD(88, true, ctis_fwd_m88_v)
+CTIS_FWD(88, false, ctis_fwd_m88_s)
+CTIS_FWD(96, true, ctis_fwd_m96_v)
 CTIS_FWD(96, false, ctis_fwd_m96_s)
 
 extern "C" __global__ void __launch_bounds__(kBackThreads, 2) ctis_back_v(const TabArgs A) { back_body<true>(A); }
