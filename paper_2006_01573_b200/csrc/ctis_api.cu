@@ -85,6 +85,7 @@ struct ctis_plan_s {
   int64_t band_begin = 0, band_end = 0, total_taps = 0;
   bool shard = false, validate = true, use_graph = true;
   bool vec_f = false, vec_b = false;
+  int back_nb = kBackBandsMax;
   std::vector<Page> fwd, back;
   float* d_hband = nullptr;
   int* d_flag = nullptr;
@@ -136,7 +137,7 @@ struct Mode {
 };
 
 constexpr int kModeTrack = 3;   // max band-to-band move of a mode (pixels, Chebyshev)
-constexpr int kModeSpan = 12;   // max |shift| of a tap from its mode reference (pixels)
+constexpr int kModeSpan = kModeSpanMax;  // max |shift| of a tap from its mode reference (pixels)
 
 std::vector<Mode> cluster_modes(const std::vector<std::vector<TapXY>>& bands) {
   const int nb = (int)bands.size();
@@ -262,17 +263,18 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
 }
 
 // Back chunk descriptor for bands [b0, b0+nb) (local) and all modes of the chunk.
-bool back_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<Mode>& ms, const std::vector<float>& invh,
-               bool vec, std::vector<uint32_t>& out, int& tiles) {
+bool back_desc(const ctis_plan_s& P, int b0, int nb, int NB, const std::vector<Mode>& ms,
+               const std::vector<float>& invh, bool vec, std::vector<uint32_t>& out, int& tiles) {
   const int nm = (int)ms.size();
-  out.assign(kDescHeader + 4 * nm + 2 * nm * kBackBands + nb, 0u);
+  out.assign(kDescHeader + 4 * nm + 2 * nm * NB + nb, 0u);
   const int tiles_r = (P.a + kBackTR - 1) / kBackTR, tiles_c = (P.alpha + kBackTC - 1) / kBackTC;
   out[0] = (uint32_t)b0;
   out[1] = (uint32_t)nb;
   out[2] = (uint32_t)nm;
   out[3] = (uint32_t)tiles_r;
   out[4] = (uint32_t)tiles_c;
-  const int MI = kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * kBackBands;
+  out[5] = (uint32_t)NB;
+  const int MI = kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * NB;
   for (int c = 0; c < nm; ++c) {
     const Mode& md = ms[c];
     int rmin = INT_MAX, rmax = INT_MIN, cmin = INT_MAX, cmax = INT_MIN;
@@ -296,8 +298,8 @@ bool back_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<Mode>& ms
     out[MI + 4 * c + 2] = (uint32_t)WC;
     for (const ModeTap& t : md.taps) {
       const int dr = t.dr - md.ref_dr, dc = t.dc - md.ref_dc;
-      out[TP + 2 * (c * kBackBands + t.b)] = (uint32_t)(4 * ((dr - rmin + lead) + WR * (dc - cmin)));
-      out[TP + 2 * (c * kBackBands + t.b) + 1] = fbits(t.w);
+      out[TP + 2 * (c * NB + t.b)] = (uint32_t)(4 * ((dr - rmin + lead) + WR * (dc - cmin)));
+      out[TP + 2 * (c * NB + t.b) + 1] = fbits(t.w);
     }
   }
   for (int b = 0; b < nb; ++b) out[IH + b] = fbits(invh[b0 + b]);
@@ -355,10 +357,42 @@ ctis_status load_page(Page& pg, bool vec) {
   if (pg.forward) {
     name = "ctis_fwd_m" + std::to_string(pg.max_modes) + (vec ? "_v" : "_s");
   } else {
-    name = std::string("ctis_back") + (vec ? "_v" : "_s");
+    name = "ctis_back_b" + std::to_string(pg.max_modes) + (vec ? "_v" : "_s");
   }
   CTIS_CUDA(cudaLibraryGetKernel(&pg.kern, pg.lib, name.c_str()), "cudaLibraryGetKernel");
   return CTIS_OK;
+}
+
+// Split w bands into the fewest chunks of <= maxb bands, balanced (sizes differ by at most 1).
+std::vector<std::pair<int, int>> balanced_chunks(int w, int maxb) {
+  const int nch = (w + maxb - 1) / maxb;
+  std::vector<std::pair<int, int>> out;
+  int b0 = 0;
+  for (int k = 0; k < nch; ++k) {
+    const int nb = w / nch + (k < w % nch ? 1 : 0);
+    out.emplace_back(b0, nb);
+    b0 += nb;
+  }
+  return out;
+}
+
+// Back-kernel band template: minimise (waves over 2 CTAs/SM) x (NB + window cost in band units).
+int choose_back_nb(const ctis_plan_s& P) {
+  const long long tiles = (long long)((P.a + kBackTR - 1) / kBackTR) * ((P.alpha + kBackTC - 1) / kBackTC);
+  const long long slots = 148LL * 2;
+  int best = kBackBandsMax;
+  double bestc = 1e300;
+  for (int NB : {16, 12, 8, 4}) {
+    const long long nch = (P.w + NB - 1) / NB;
+    const long long ctas = tiles * nch;
+    const double waves = std::ceil((double)ctas / (double)slots);
+    const double c = waves * (NB + 5.0);
+    if (c < bestc - 1e-9) {
+      bestc = c;
+      best = NB;
+    }
+  }
+  return best;
 }
 
 ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& bands, const std::vector<float>& invh) {
@@ -368,9 +402,9 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
   //      up to 8) for the whole plan so that every forward page runs the same kernel template
   {
     std::vector<std::vector<Mode>> chunk_modes;
+    std::vector<std::pair<int, int>> chunks = balanced_chunks(P.w, kFwdBands);
     int maxm = 8;
-    for (int b0 = 0; b0 < P.w; b0 += kFwdBands) {
-      const int nb = std::min(kFwdBands, P.w - b0);
+    for (auto [b0, nb] : chunks) {
       std::vector<std::vector<TapXY>> cb(bands.begin() + b0, bands.begin() + b0 + nb);
       chunk_modes.push_back(cluster_modes(cb));
       maxm = std::max(maxm, std::min(96, ((int)chunk_modes.back().size() + 7) / 8 * 8));
@@ -378,7 +412,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     std::vector<std::vector<uint32_t>> descs;
     std::vector<int> tiles, modes;
     for (size_t k = 0; k < chunk_modes.size(); ++k) {
-      const int b0 = (int)k * kFwdBands, nb = std::min(kFwdBands, P.w - b0);
+      const int b0 = chunks[k].first, nb = chunks[k].second;
       const std::vector<Mode>& ms = chunk_modes[k];
       for (size_t s0 = 0; s0 < ms.size(); s0 += (size_t)maxm) {
         std::vector<const Mode*> pass;
@@ -394,32 +428,33 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     }
     pack_pages(P.fwd, true, descs, tiles, modes);
   }
-  // ---- back: chunks of up to kBackBands bands (fewer if a descriptor would not fit a page)
+  // ---- back: NB (kernel template) chosen so that tiles x chunks fills the SMs; a chunk whose
+  //      descriptor would not fit one 64 KB page is split further
   {
+    P.back_nb = choose_back_nb(P);
     std::vector<std::vector<uint32_t>> descs;
     std::vector<int> tiles, modes;
-    int b0 = 0;
-    while (b0 < P.w) {
-      int nb = std::min(kBackBands, P.w - b0);
-      for (;;) {
-        std::vector<std::vector<TapXY>> cb(bands.begin() + b0, bands.begin() + b0 + nb);
-        std::vector<Mode> ms = cluster_modes(cb);
-        std::vector<uint32_t> d;
-        int t = 0;
-        if (!back_desc(P, b0, nb, ms, invh, P.vec_b, d, t)) return fail(CTIS_ERR_TAP, "back window overflow");
-        if ((int)d.size() + kPageHeader <= kPageWords || nb == 1) {
-          if ((int)d.size() + kPageHeader > kPageWords)
-            return fail(CTIS_ERR_TAP, "band has too many taps for one 64 KB tap page");
-          descs.push_back(std::move(d));
-          tiles.push_back(t);
-          modes.push_back((int)ms.size());
-          break;
-        }
-        nb = (nb + 1) / 2;
+    std::vector<std::pair<int, int>> todo = balanced_chunks(P.w, P.back_nb);
+    for (size_t k = 0; k < todo.size(); ++k) {
+      const int b0 = todo[k].first, nb = todo[k].second;
+      std::vector<std::vector<TapXY>> cb(bands.begin() + b0, bands.begin() + b0 + nb);
+      std::vector<Mode> ms = cluster_modes(cb);
+      std::vector<uint32_t> d;
+      int t = 0;
+      if (!back_desc(P, b0, nb, P.back_nb, ms, invh, P.vec_b, d, t)) return fail(CTIS_ERR_TAP, "back window overflow");
+      if ((int)d.size() + kPageHeader > kPageWords) {
+        if (nb == 1) return fail(CTIS_ERR_TAP, "band has too many taps for one 64 KB tap page");
+        todo.insert(todo.begin() + (long)k + 1, {b0 + nb / 2, nb - nb / 2});
+        todo[k].second = nb / 2;
+        --k;
+        continue;
       }
-      b0 += nb;
+      descs.push_back(std::move(d));
+      tiles.push_back(t);
+      modes.push_back((int)ms.size());
     }
-    pack_pages(P.back, false, descs, tiles, modes);
+    std::vector<int> nbs(descs.size(), P.back_nb);  // back pages: "max_modes" carries NB
+    pack_pages(P.back, false, descs, tiles, nbs);
   }
   for (Page& pg : P.fwd) {
     ctis_status st = load_page(pg, P.vec_f);
@@ -548,7 +583,7 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
     dim3 grid(pg.max_tiles, pg.nchunks, frames);
     void* args[] = {&A};
     const int threads = pg.forward ? kFwdThreads : kBackThreads;
-    const size_t smem = 2 * sizeof(float) * (pg.forward ? kFwdWinFloats : kBackWinFloats);
+    const size_t smem = kStages * sizeof(float) * (pg.forward ? kFwdWinFloats : kBackWinFloats);
     cudaError_t e = cudaLaunchKernel((const void*)pg.kern, grid, dim3(threads), args, smem, s);
     if (e != cudaSuccess) return e;
     if (count) ++*count;

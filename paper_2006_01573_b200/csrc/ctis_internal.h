@@ -25,26 +25,30 @@ constexpr int kPageWords = 16384;  // 64 KB of uint32
 //   [TP = BI+4*nb ..]   per (b, c), c < MAXM: byte offset, w-bits  (index TP + 2*(b*MAXM + c);
 //                       w = 0 -> no tap; MAXM = nm rounded up to 8 = the kernel template)
 // Back chunk descriptor (Eqs. 14-15):
-//   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] tiles_r   [D+4] tiles_c   [D+5..7] 0
+//   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] tiles_r   [D+4] tiles_c   [D+5] NB   [D+6..7] 0
 //   [MI = D+8 ..]       per mode c: Bm, WR, WC, 0    (window origin term in [0, n))
-//   [TP = MI+4*nm ..]   per (c, b), b < kBackBands: byte offset, w-bits  (index TP + 2*(c*kBackBands + b))
-//   [IH = TP+2*nm*kBackBands ..] inv_h[b]
+//   [TP = MI+4*nm ..]   per (c, b), b < NB: byte offset, w-bits  (index TP + 2*(c*NB + b))
+//   [IH = TP+2*nm*NB ..] inv_h[b]
 enum : int { kDescHeader = 8 };
 
 // Forward kernel geometry: one u-space position per thread, 32 rows x 16 columns per CTA.
 constexpr int kFwdTR = 32;
 constexpr int kFwdTC = 16;
 constexpr int kFwdThreads = kFwdTR * kFwdTC;
-constexpr int kFwdBands = 16;           // bands per forward chunk
-// Back kernel geometry: 32 x 32 voxel tile, 2 voxels per thread, kBackBands bands.
+constexpr int kFwdBands = 16;           // max bands per forward chunk (chunks are balanced)
+// Back kernel geometry: 32 x 32 voxel tile, 2 voxels per thread, NB in {4, 8, 12, 16} bands
+// per chunk (kernel template; the plan picks the one that fills the 148 SMs best).
 constexpr int kBackTR = 32;
 constexpr int kBackTC = 32;
 constexpr int kBackThreads = 512;
-constexpr int kBackBands = 16;
+constexpr int kBackBandsMax = 16;
 
-// Shared-memory window capacity (floats per buffer, two buffers per CTA).
-constexpr int kFwdWinFloats = 5120;     // 20 KB
-constexpr int kBackWinFloats = 5120;
+// Mode shifts are bounded by kModeSpan (|dr|, |dc| <= 12 from the mode reference), so a window
+// never exceeds (32 + 24 + 3 -> 60) x (16 + 24) floats (forward) or 60 x (32 + 24) (back).
+constexpr int kModeSpanMax = 12;
+constexpr int kStages = 3;              // window pipeline depth (cp.async groups in flight)
+constexpr int kFwdWinFloats = 2560;     // 10 KB per stage
+constexpr int kBackWinFloats = 3584;    // 14 KB per stage
 
 // Per-launch parameters of the table kernels.
 struct TabArgs {

@@ -56,51 +56,63 @@ __device__ __forceinline__ void cp_wait() {
 __device__ __forceinline__ int tabi(uint32_t i) { return (int)c_tab[i]; }
 __device__ __forceinline__ float tabf(uint32_t i) { return __uint_as_float(c_tab[i]); }
 
+// Window loaders.  A window is WR x WC floats (WR <= 64, WR % 4 == 0 on the 16-byte path),
+// stored column by column with pitch WR.  Lanes 0-15 copy 16 four-float chunks of one window
+// column, lanes 16-31 the next column, so a warp covers two columns per pass (32-bit math only).
+
 // f_lam window: element (i, j) = f_lam[(row0 + i) + a*(col0 + j)], zero outside the field stop.
-template <bool VEC>
+template <int NWARPS, bool VEC>
 __device__ __forceinline__ void load_f_window(float* buf, const float* fl, const TabArgs& A, int row0, int col0,
                                               int WR, int WC) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int NW = kFwdThreads / 32;
-  for (int j = warp; j < WC; j += NW) {
-    const int cc = col0 + j;
-    const bool cok = (cc >= 0) & (cc < A.alpha);
-    const float* col = fl + (long long)A.a * cc;
-    if (VEC) {
-      for (int i = lane * 4; i < WR; i += 128) {
-        const int rr = row0 + i;
-        const bool ok = cok & (rr >= 0) & (rr < A.a);
-        cp_async16(buf + i + WR * j, ok ? col + rr : fl, ok);
-      }
-    } else {
+  if (VEC) {
+    const int i = (lane & 15) * 4, rr = row0 + i;
+    const bool rok = (i < WR) & (rr >= 0) & (rr < A.a);
+    for (int j = 2 * warp + (lane >> 4); j < WC; j += 2 * NWARPS) {
+      const int cc = col0 + j;
+      const bool ok = rok & (cc >= 0) & (cc < A.alpha);
+      if (i < WR) cp_async16(buf + i + WR * j, ok ? fl + rr + A.a * cc : fl, ok);
+    }
+  } else {
+    for (int j = warp; j < WC; j += NWARPS) {
+      const int cc = col0 + j;
+      const bool cok = (cc >= 0) & (cc < A.alpha);
       for (int i = lane; i < WR; i += 32) {
         const int rr = row0 + i;
         const bool ok = cok & (rr >= 0) & (rr < A.a);
-        cp_async4(buf + i + WR * j, ok ? col + rr : fl, ok);
+        cp_async4(buf + i + WR * j, ok ? fl + rr + A.a * cc : fl, ok);
       }
     }
   }
 }
 
-// r window: element (i, j) = r[(B + i + gamma*j) mod n]  (B in [0, n)).
-template <bool VEC>
-__device__ __forceinline__ void load_r_window(float* buf, const float* r, const TabArgs& A, long long B, int WR,
+// r window: element (i, j) = r[(B + i + gamma*j) mod n]  (0 <= B < n).
+template <int NWARPS, bool VEC>
+__device__ __forceinline__ void load_r_window(float* buf, const float* r, const TabArgs& A, unsigned B, int WR,
                                               int WC) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int NW = kBackThreads / 32;
-  for (int j = warp; j < WC; j += NW) {
-    long long cb = B + (long long)A.gamma * j;
-    if (cb >= A.n) cb %= A.n;
-    if (VEC) {
-      for (int i = lane * 4; i < WR; i += 128) {
-        long long idx = cb + i;
-        if (idx >= A.n) idx %= A.n;
-        cp_async16(buf + i + WR * j, r + idx, true);
-      }
-    } else {
+  const unsigned n = (unsigned)A.n;
+  if (VEC) {
+    const int i = (lane & 15) * 4;
+    if (i >= WR) return;
+    const int j0 = 2 * warp + (lane >> 4);
+    unsigned cb = B + (unsigned)A.gamma * (unsigned)j0;
+    while (cb >= n) cb -= n;
+    const unsigned step = (unsigned)A.gamma * (2u * NWARPS);
+    for (int j = j0; j < WC; j += 2 * NWARPS) {
+      unsigned idx = cb + (unsigned)i;
+      while (idx >= n) idx -= n;
+      cp_async16(buf + i + WR * j, r + idx, true);
+      cb += step;
+      while (cb >= n) cb -= n;
+    }
+  } else {
+    for (int j = warp; j < WC; j += NWARPS) {
+      unsigned cb = B + (unsigned)((unsigned long long)A.gamma * (unsigned)j % n);
+      while (cb >= n) cb -= n;
       for (int i = lane; i < WR; i += 32) {
-        long long idx = cb + i;
-        if (idx >= A.n) idx %= A.n;
+        unsigned idx = cb + (unsigned)i;
+        while (idx >= n) idx -= n;
         cp_async4(buf + i + WR * j, r + idx, true);
       }
     }
@@ -131,25 +143,29 @@ __device__ __forceinline__ void forward_body(const TabArgs& A) {
 #pragma unroll
   for (int c = 0; c < MAXM; ++c) acc[c] = 0.f;
 
-  load_f_window<VEC>(smem, f + (long long)lam0 * A.ell, A, U_r + tabi(BI + 0), U_c + tabi(BI + 1), tabi(BI + 2),
-                     tabi(BI + 3));
-  cp_commit();
-  for (int b = 0; b < nb; ++b) {
-    if (b + 1 < nb) {
-      const uint32_t bi = BI + 4 * (b + 1);
-      load_f_window<VEC>(smem + ((b + 1) & 1) * kFwdWinFloats, f + (long long)(lam0 + b + 1) * A.ell, A,
-                         U_r + tabi(bi + 0), U_c + tabi(bi + 1), tabi(bi + 2), tabi(bi + 3));
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
+  auto issue = [&](int b) {
+    if (b < nb) {
+      const uint32_t bi = BI + 4 * b;
+      load_f_window<kFwdThreads / 32, VEC>(smem + (b % kStages) * kFwdWinFloats, f + (long long)(lam0 + b) * A.ell, A,
+                                           U_r + tabi(bi + 0), U_c + tabi(bi + 1), tabi(bi + 2), tabi(bi + 3));
     }
+    cp_commit();  // one (possibly empty) group per band keeps the group arithmetic uniform
+  };
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) issue(s);
+  for (int b = 0; b < nb; ++b) {
+    issue(b + kStages - 1);
+    cp_wait<kStages - 1>();
     __syncthreads();
     // byte address of this thread's u in the window; tap entries hold byte offsets (absent: w = 0)
-    const unsigned base = sbase + 4u * ((b & 1) * kFwdWinFloats + lane + tabi(BI + 4 * b + 2) * warp);
-    const uint32_t tp = TP + 2 * b * MAXM;
+    const unsigned base = sbase + 4u * ((b % kStages) * kFwdWinFloats + lane + tabi(BI + 4 * b + 2) * warp);
+    // pointer arithmetic (not an unsigned index) lets ptxas fold 8*c into LDCU.64 c[0x3][UR+imm]
+    const uint2* ent = reinterpret_cast<const uint2*>(c_tab + TP) + b * MAXM;
 #pragma unroll
-    for (int c = 0; c < MAXM; ++c) acc[c] = fmaf(tabf(tp + 2 * c + 1), lds(base + c_tab[tp + 2 * c]), acc[c]);
+    for (int c = 0; c < MAXM; ++c) {
+      const uint2 e = ent[c];
+      acc[c] = fmaf(__uint_as_float(e.y), lds(base + e.x), acc[c]);
+    }
     __syncthreads();
   }
   float* g = A.dst + (long long)blockIdx.z * A.dst_frame;
@@ -164,7 +180,7 @@ __device__ __forceinline__ void forward_body(const TabArgs& A) {
   }
 }
 
-template <bool VEC>
+template <int NB, bool VEC>
 __device__ __forceinline__ void back_body(const TabArgs& A) {
   extern __shared__ __align__(16) float smem[];
   const uint32_t D = c_tab[1 + blockIdx.y];
@@ -175,41 +191,41 @@ __device__ __forceinline__ void back_body(const TabArgs& A) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q_r0 = (tile % tiles_r) * kBackTR, q_c0 = (tile / tiles_r) * kBackTC;
   const float* r = A.src + (long long)blockIdx.z * A.src_frame;
-  const uint32_t MI = D + kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * kBackBands;
+  const uint32_t MI = D + kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * NB;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
-  const long long tile1d = (long long)q_r0 + (long long)A.gamma * q_c0;
+  const unsigned tile1d = (unsigned)(q_r0 + A.gamma * q_c0);  // < n
 
-  float acc0[kBackBands], acc1[kBackBands];
+  float acc0[NB], acc1[NB];
 #pragma unroll
-  for (int b = 0; b < kBackBands; ++b) acc0[b] = acc1[b] = 0.f;
+  for (int b = 0; b < NB; ++b) acc0[b] = acc1[b] = 0.f;
 
   auto origin = [&](int c) {
-    long long B = tile1d + tabi(MI + 4 * c);
-    if (B >= A.n) B %= A.n;
+    unsigned B = tile1d + c_tab[MI + 4 * c];
+    while (B >= (unsigned)A.n) B -= (unsigned)A.n;
     return B;
   };
-  load_r_window<VEC>(smem, r, A, origin(0), tabi(MI + 1), tabi(MI + 2));
-  cp_commit();
+  auto issue = [&](int c) {
+    if (c < nm)
+      load_r_window<kBackThreads / 32, VEC>(smem + (c % kStages) * kBackWinFloats, r, A, origin(c),
+                                            tabi(MI + 4 * c + 1), tabi(MI + 4 * c + 2));
+    cp_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) issue(s);
   for (int c = 0; c < nm; ++c) {
-    if (c + 1 < nm) {
-      load_r_window<VEC>(smem + ((c + 1) & 1) * kBackWinFloats, r, A, origin(c + 1), tabi(MI + 4 * (c + 1) + 1),
-                         tabi(MI + 4 * (c + 1) + 2));
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
+    issue(c + kStages - 1);
+    cp_wait<kStages - 1>();
     __syncthreads();
     const int WR = tabi(MI + 4 * c + 1);
-    const unsigned b0a = sbase + 4u * ((c & 1) * kBackWinFloats + lane + WR * warp);
+    const unsigned b0a = sbase + 4u * ((c % kStages) * kBackWinFloats + lane + WR * warp);
     const unsigned b1a = b0a + 4u * WR * (kBackThreads / 32);
-    const uint32_t tp = TP + 2 * c * kBackBands;
+    const uint2* ent = reinterpret_cast<const uint2*>(c_tab + TP) + c * NB;
 #pragma unroll
-    for (int b = 0; b < kBackBands; ++b) {
-      const float w = tabf(tp + 2 * b + 1);
-      const unsigned off = c_tab[tp + 2 * b];
-      acc0[b] = fmaf(w, lds(b0a + off), acc0[b]);
-      acc1[b] = fmaf(w, lds(b1a + off), acc1[b]);
+    for (int b = 0; b < NB; ++b) {
+      const uint2 e = ent[b];
+      const float w = __uint_as_float(e.y);
+      acc0[b] = fmaf(w, lds(b0a + e.x), acc0[b]);
+      acc1[b] = fmaf(w, lds(b1a + e.x), acc1[b]);
     }
     __syncthreads();
   }
@@ -217,7 +233,7 @@ __device__ __forceinline__ void back_body(const TabArgs& A) {
   const int qr = q_r0 + lane, qc0 = q_c0 + warp, qc1 = qc0 + kBackThreads / 32;
   if (qr >= A.a) return;
 #pragma unroll
-  for (int b = 0; b < kBackBands; ++b) {
+  for (int b = 0; b < NB; ++b) {
     if (b < nb) {
       const long long lb = (long long)(lam0 + b) * A.ell + qr;
       const float ih = tabf(IH + b);
@@ -262,5 +278,13 @@ CTIS_FWD(88, false, ctis_fwd_m88_s)
 CTIS_FWD(96, true, ctis_fwd_m96_v)
 CTIS_FWD(96, false, ctis_fwd_m96_s)
 
-extern "C" __global__ void __launch_bounds__(kBackThreads, 2) ctis_back_v(const TabArgs A) { back_body<true>(A); }
-extern "C" __global__ void __launch_bounds__(kBackThreads, 2) ctis_back_s(const TabArgs A) { back_body<false>(A); }
+#define CTIS_BACK(NB, V, NAME) \
+  extern "C" __global__ void __launch_bounds__(kBackThreads, 2) NAME(const TabArgs A) { back_body<NB, V>(A); }
+CTIS_BACK(4, true, ctis_back_b4_v)
+CTIS_BACK(4, false, ctis_back_b4_s)
+CTIS_BACK(8, true, ctis_back_b8_v)
+CTIS_BACK(8, false, ctis_back_b8_s)
+CTIS_BACK(12, true, ctis_back_b12_v)
+CTIS_BACK(12, false, ctis_back_b12_s)
+CTIS_BACK(16, true, ctis_back_b16_v)
+CTIS_BACK(16, false, ctis_back_b16_s)
