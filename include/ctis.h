@@ -22,7 +22,7 @@
  *
  * Conventions for every entry point:
  *   - sizes are int64_t; n = gamma*xi, l = a*alpha, m = l*w (or l*(band_end-band_begin)
- *     for a shard plan, "m_local"); n and m must be < 2^31.
+ *     for a shard plan, "m_local"); n must be < 2^30 and m < 2^31.
  *   - float* arguments of the stream-ordered calls are DEVICE pointers on the plan's
  *     device, owned by the caller, 16-byte aligned, non-overlapping unless stated.
  *     The plan owns only its tap tables and a few bytes of scratch.
@@ -59,7 +59,7 @@ typedef enum {
   CTIS_OK = 0,
   CTIS_ERR_INVALID_ARGUMENT = 1, /* null pointer, iters < 0, frames < 1, misaligned pointer,
                                     wrong call for the plan kind (mlem on a shard plan) */
-  CTIS_ERR_DIMENSION = 2,        /* a, alpha, w, gamma, xi < 1; gamma < a; xi < alpha; n or m >= 2^31;
+  CTIS_ERR_DIMENSION = 2,        /* a, alpha, w, gamma, xi < 1; gamma < a; xi < alpha; n >= 2^30; m >= 2^31;
                                     band range outside [0, w) or empty */
   CTIS_ERR_TAP = 3,              /* tap_ptr not a CSR over w bands; offset outside [0, n);
                                     weight <= 0 or non-finite; duplicate offset within a band;

@@ -1,6 +1,7 @@
 // ctis_api.cu — the C ABI of libctis (include/ctis.h): plan builder (tap validation,
 // mode clustering, __constant__ tap pages), stream-ordered entry points, CUDA-graph
 // replay of the MLEM iterations.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -84,8 +85,9 @@ struct ctis_plan_s {
   int a = 0, alpha = 0, w = 0, gamma = 0, xi = 0, n = 0, ell = 0, m = 0;
   int64_t band_begin = 0, band_end = 0, total_taps = 0;
   bool shard = false, validate = true, use_graph = true;
-  bool vec_f = false, vec_b = false;
+  bool tma_f = false, tma_b = false;
   int back_nb = kBackBandsMax;
+  int fbox_r = 0, fbox_c = 0, bbox_r = 0, bbox_c = 0;
   std::vector<Page> fwd, back;
   float* d_hband = nullptr;
   int* d_flag = nullptr;
@@ -192,7 +194,6 @@ std::vector<Mode> cluster_modes(const std::vector<std::vector<TapXY>>& bands) {
   return modes;
 }
 
-inline int mod4(long long x) { return (int)(((x % 4) + 4) % 4); }
 inline int round4(int x) { return (x + 3) & ~3; }
 inline uint32_t fbits(float x) {
   uint32_t u;
@@ -200,61 +201,78 @@ inline uint32_t fbits(float x) {
   return u;
 }
 
-// Forward chunk descriptor for bands [b0, b0+nb) (local) and the given modes.
-bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const Mode*>& ms, int maxm, bool vec,
-                  std::vector<uint32_t>& out, int& tiles) {
-  const int nm = (int)ms.size();
-  std::vector<int> rmin(nb, INT_MAX), rmax(nb, INT_MIN), cmin(nb, INT_MAX), cmax(nb, INT_MIN);
-  int Rmin = INT_MAX, Rmax = INT_MIN, Cmin = INT_MAX, Cmax = INT_MIN;
+// Per-band (forward) or per-mode (back) shift ranges.
+struct Span {
+  int rmin = INT_MAX, rmax = INT_MIN, cmin = INT_MAX, cmax = INT_MIN;
+  void add(int dr, int dc) {
+    rmin = std::min(rmin, dr);
+    rmax = std::max(rmax, dr);
+    cmin = std::min(cmin, dc);
+    cmax = std::max(cmax, dc);
+  }
+  bool empty() const { return rmin == INT_MAX; }
+};
+
+std::vector<Span> band_spans(int nb, const std::vector<const Mode*>& ms) {
+  std::vector<Span> sp(nb);
   for (const Mode* md : ms)
-    for (const ModeTap& t : md->taps) {
-      const int dr = t.dr - md->ref_dr, dc = t.dc - md->ref_dc;
-      rmin[t.b] = std::min(rmin[t.b], dr);
-      rmax[t.b] = std::max(rmax[t.b], dr);
-      cmin[t.b] = std::min(cmin[t.b], dc);
-      cmax[t.b] = std::max(cmax[t.b], dc);
-      Rmin = std::min(Rmin, dr);
-      Rmax = std::max(Rmax, dr);
-      Cmin = std::min(Cmin, dc);
-      Cmax = std::max(Cmax, dc);
+    for (const ModeTap& t : md->taps) sp[t.b].add(t.dr - md->ref_dr, t.dc - md->ref_dc);
+  return sp;
+}
+
+Span mode_span(const Mode& md) {
+  Span s;
+  for (const ModeTap& t : md.taps) s.add(t.dr - md.ref_dr, t.dc - md.ref_dc);
+  return s;
+}
+
+// Forward chunk descriptor for bands [b0, b0+nb) (local) and the given modes.  box_r > 0 selects
+// the TMA layout (every window is a box_r x box_c box with pitch box_r); box_r == 0 the element
+// loader layout (exact per-band window, pitch = its own row count).
+bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const Mode*>& ms, int maxm, int box_r,
+                  int box_c, std::vector<uint32_t>& out, int& tiles) {
+  const int nm = (int)ms.size();
+  const std::vector<Span> sp = band_spans(nb, ms);
+  Span all;
+  for (const Span& x : sp)
+    if (!x.empty()) {
+      all.add(x.rmin, x.cmin);
+      all.add(x.rmax, x.cmax);
     }
-  if (Rmin == INT_MAX) return true;  // no taps: nothing to emit
-  const int u_r0 = Rmin, u_c0 = Cmin;
-  const int tiles_r = (P.a + Rmax - Rmin + kFwdTR - 1) / kFwdTR;
-  const int tiles_c = (P.alpha + Cmax - Cmin + kFwdTC - 1) / kFwdTC;
+  if (all.empty()) return true;  // no taps: nothing to emit
+  const int tiles_r = (P.a + all.rmax - all.rmin + kFwdTR - 1) / kFwdTR;
+  const int tiles_c = (P.alpha + all.cmax - all.cmin + kFwdTC - 1) / kFwdTC;
   out.assign(kDescHeader + nm + 4 * nb + 2 * nb * maxm, 0u);
   out[0] = (uint32_t)b0;
   out[1] = (uint32_t)nb;
   out[2] = (uint32_t)nm;
-  out[3] = (uint32_t)u_r0;
-  out[4] = (uint32_t)u_c0;
+  out[3] = (uint32_t)all.rmin;
+  out[4] = (uint32_t)all.cmin;
   out[5] = (uint32_t)tiles_r;
   out[6] = (uint32_t)tiles_c;
   out[7] = (uint32_t)maxm;
   for (int c = 0; c < nm; ++c) out[kDescHeader + c] = (uint32_t)(ms[c]->ref_dr + P.gamma * ms[c]->ref_dc);
   const int BI = kDescHeader + nm, TP = BI + 4 * nb;
-  std::vector<int> WRs(nb, 4), lead(nb, 0);
+  std::vector<int> WRs(nb, 1);
   for (int b = 0; b < nb; ++b) {
-    if (rmin[b] == INT_MAX) {  // band without taps in this pass: empty window
-      out[BI + 4 * b + 2] = 4;
-      out[BI + 4 * b + 3] = 0;
+    if (sp[b].empty()) {  // band without taps in this pass: any window, never read
+      out[BI + 4 * b + 2] = (uint32_t)std::max(box_r, 1);
+      out[BI + 4 * b + 3] = box_r ? (uint32_t)box_c : 0u;
       continue;
     }
-    lead[b] = vec ? mod4((long long)u_r0 - rmax[b]) : 0;
-    int WR = kFwdTR + rmax[b] - rmin[b] + lead[b];
-    if (vec) WR = round4(WR);
-    const int WC = kFwdTC + cmax[b] - cmin[b];
+    const int WR = box_r ? box_r : kFwdTR + sp[b].rmax - sp[b].rmin;
+    const int WC = box_r ? box_c : kFwdTC + sp[b].cmax - sp[b].cmin;
     if (WR * WC > kFwdWinFloats) return false;
     WRs[b] = WR;
-    out[BI + 4 * b + 0] = (uint32_t)(-rmax[b] - lead[b]);
-    out[BI + 4 * b + 1] = (uint32_t)(-cmax[b]);
+    out[BI + 4 * b + 0] = (uint32_t)(-sp[b].rmax);
+    out[BI + 4 * b + 1] = (uint32_t)(-sp[b].cmax);
     out[BI + 4 * b + 2] = (uint32_t)WR;
     out[BI + 4 * b + 3] = (uint32_t)WC;
   }
   for (int c = 0; c < nm; ++c)
     for (const ModeTap& t : ms[c]->taps) {
       const int dr = t.dr - ms[c]->ref_dr, dc = t.dc - ms[c]->ref_dc;
-      const int off = (rmax[t.b] + lead[t.b] - dr) + WRs[t.b] * (cmax[t.b] - dc);
+      const int off = (sp[t.b].rmax - dr) + WRs[t.b] * (sp[t.b].cmax - dc);
       out[TP + 2 * (t.b * maxm + c)] = (uint32_t)(4 * off);
       out[TP + 2 * (t.b * maxm + c) + 1] = fbits(t.w);
     }
@@ -262,9 +280,9 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
   return true;
 }
 
-// Back chunk descriptor for bands [b0, b0+nb) (local) and all modes of the chunk.
+// Back chunk descriptor for bands [b0, b0+nb) (local) and all modes of the chunk (same layouts).
 bool back_desc(const ctis_plan_s& P, int b0, int nb, int NB, const std::vector<Mode>& ms,
-               const std::vector<float>& invh, bool vec, std::vector<uint32_t>& out, int& tiles) {
+               const std::vector<float>& invh, int box_r, int box_c, std::vector<uint32_t>& out, int& tiles) {
   const int nm = (int)ms.size();
   out.assign(kDescHeader + 4 * nm + 2 * nm * NB + nb, 0u);
   const int tiles_r = (P.a + kBackTR - 1) / kBackTR, tiles_c = (P.alpha + kBackTC - 1) / kBackTC;
@@ -277,28 +295,19 @@ bool back_desc(const ctis_plan_s& P, int b0, int nb, int NB, const std::vector<M
   const int MI = kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * NB;
   for (int c = 0; c < nm; ++c) {
     const Mode& md = ms[c];
-    int rmin = INT_MAX, rmax = INT_MIN, cmin = INT_MAX, cmax = INT_MIN;
-    for (const ModeTap& t : md.taps) {
-      rmin = std::min(rmin, t.dr - md.ref_dr);
-      rmax = std::max(rmax, t.dr - md.ref_dr);
-      cmin = std::min(cmin, t.dc - md.ref_dc);
-      cmax = std::max(cmax, t.dc - md.ref_dc);
-    }
+    const Span sp = mode_span(md);
     const long long oref = (long long)md.ref_dr + (long long)P.gamma * md.ref_dc;
-    const long long B0 = oref + rmin + (long long)P.gamma * cmin;
-    const int lead = vec ? mod4(B0) : 0;
-    long long Bm = (B0 - lead) % P.n;
+    long long Bm = (oref + sp.rmin + (long long)P.gamma * sp.cmin) % P.n;
     if (Bm < 0) Bm += P.n;
-    int WR = kBackTR + rmax - rmin + lead;
-    if (vec) WR = round4(WR);
-    const int WC = kBackTC + cmax - cmin;
+    const int WR = box_r ? box_r : kBackTR + sp.rmax - sp.rmin;
+    const int WC = box_r ? box_c : kBackTC + sp.cmax - sp.cmin;
     if (WR * WC > kBackWinFloats) return false;
     out[MI + 4 * c + 0] = (uint32_t)Bm;
     out[MI + 4 * c + 1] = (uint32_t)WR;
     out[MI + 4 * c + 2] = (uint32_t)WC;
     for (const ModeTap& t : md.taps) {
       const int dr = t.dr - md.ref_dr, dc = t.dc - md.ref_dc;
-      out[TP + 2 * (c * NB + t.b)] = (uint32_t)(4 * ((dr - rmin + lead) + WR * (dc - cmin)));
+      out[TP + 2 * (c * NB + t.b)] = (uint32_t)(4 * ((dr - sp.rmin) + WR * (dc - sp.cmin)));
       out[TP + 2 * (c * NB + t.b) + 1] = fbits(t.w);
     }
   }
@@ -355,9 +364,9 @@ ctis_status load_page(Page& pg, bool vec) {
   CTIS_CUDA(cudaMemcpy(dptr, pg.words.data(), pg.words.size() * 4, cudaMemcpyHostToDevice), "upload tap page");
   std::string name;
   if (pg.forward) {
-    name = "ctis_fwd_m" + std::to_string(pg.max_modes) + (vec ? "_v" : "_s");
+    name = "ctis_fwd_m" + std::to_string(pg.max_modes) + (vec ? "_t" : "_s");
   } else {
-    name = "ctis_back_b" + std::to_string(pg.max_modes) + (vec ? "_v" : "_s");
+    name = "ctis_back_b" + std::to_string(pg.max_modes) + (vec ? "_t" : "_s");
   }
   CTIS_CUDA(cudaLibraryGetKernel(&pg.kern, pg.lib, name.c_str()), "cudaLibraryGetKernel");
   return CTIS_OK;
@@ -396,10 +405,11 @@ int choose_back_nb(const ctis_plan_s& P) {
 }
 
 ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& bands, const std::vector<float>& invh) {
-  P.vec_f = (P.a % 4 == 0);
-  P.vec_b = (P.gamma % 4 == 0);
-  // ---- forward: chunks of kFwdBands bands, modes split into passes of <= 96; one MAXM (nm rounded
-  //      up to 8) for the whole plan so that every forward page runs the same kernel template
+  // TMA needs 16-byte global strides: a % 4 == 0 for f, gamma % 4 == 0 for r.
+  P.tma_f = (P.a % 4 == 0);
+  P.tma_b = (P.gamma % 4 == 0);
+  // ---- forward: chunks of <= kFwdBands bands, modes split into passes of <= 96; one MAXM (nm rounded
+  //      up to 8) and one TMA box for the whole plan so that every forward page runs the same kernel
   {
     std::vector<std::vector<Mode>> chunk_modes;
     std::vector<std::pair<int, int>> chunks = balanced_chunks(P.w, kFwdBands);
@@ -409,22 +419,40 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
       chunk_modes.push_back(cluster_modes(cb));
       maxm = std::max(maxm, std::min(96, ((int)chunk_modes.back().size() + 7) / 8 * 8));
     }
+    std::vector<std::vector<const Mode*>> passes;
+    std::vector<int> pass_chunk;
+    for (size_t k = 0; k < chunk_modes.size(); ++k)
+      for (size_t s0 = 0; s0 < chunk_modes[k].size(); s0 += (size_t)maxm) {
+        std::vector<const Mode*> pass;
+        for (size_t c = s0; c < std::min(chunk_modes[k].size(), s0 + (size_t)maxm); ++c) pass.push_back(&chunk_modes[k][c]);
+        passes.push_back(std::move(pass));
+        pass_chunk.push_back((int)k);
+      }
+    int box_r = 0, box_c = 0;
+    if (P.tma_f) {
+      for (size_t i = 0; i < passes.size(); ++i)
+        for (const Span& x : band_spans(chunks[pass_chunk[i]].second, passes[i]))
+          if (!x.empty()) {
+            box_r = std::max(box_r, kFwdTR + x.rmax - x.rmin);
+            box_c = std::max(box_c, kFwdTC + x.cmax - x.cmin);
+          }
+      box_r = std::max(4, round4(box_r));
+      box_c = std::max(1, box_c);
+    }
+    P.fbox_r = box_r;
+    P.fbox_c = box_c;
     std::vector<std::vector<uint32_t>> descs;
     std::vector<int> tiles, modes;
-    for (size_t k = 0; k < chunk_modes.size(); ++k) {
-      const int b0 = chunks[k].first, nb = chunks[k].second;
-      const std::vector<Mode>& ms = chunk_modes[k];
-      for (size_t s0 = 0; s0 < ms.size(); s0 += (size_t)maxm) {
-        std::vector<const Mode*> pass;
-        for (size_t c = s0; c < std::min(ms.size(), s0 + (size_t)maxm); ++c) pass.push_back(&ms[c]);
-        std::vector<uint32_t> d;
-        int t = 0;
-        if (!forward_desc(P, b0, nb, pass, maxm, P.vec_f, d, t)) return fail(CTIS_ERR_TAP, "forward window overflow");
-        if (d.empty()) continue;
-        descs.push_back(std::move(d));
-        tiles.push_back(t);
-        modes.push_back(maxm);
-      }
+    for (size_t i = 0; i < passes.size(); ++i) {
+      const int b0 = chunks[pass_chunk[i]].first, nb = chunks[pass_chunk[i]].second;
+      std::vector<uint32_t> d;
+      int t = 0;
+      if (!forward_desc(P, b0, nb, passes[i], maxm, box_r, box_c, d, t))
+        return fail(CTIS_ERR_TAP, "forward window overflow");
+      if (d.empty()) continue;
+      descs.push_back(std::move(d));
+      tiles.push_back(t);
+      modes.push_back(maxm);
     }
     pack_pages(P.fwd, true, descs, tiles, modes);
   }
@@ -432,36 +460,58 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
   //      descriptor would not fit one 64 KB page is split further
   {
     P.back_nb = choose_back_nb(P);
-    std::vector<std::vector<uint32_t>> descs;
-    std::vector<int> tiles, modes;
     std::vector<std::pair<int, int>> todo = balanced_chunks(P.w, P.back_nb);
+    std::vector<std::vector<Mode>> cms;
+    for (auto [b0, nb] : todo) {
+      std::vector<std::vector<TapXY>> cb(bands.begin() + b0, bands.begin() + b0 + nb);
+      cms.push_back(cluster_modes(cb));
+    }
+    int box_r = 0, box_c = 0;
+    if (P.tma_b) {
+      for (const auto& ms : cms)
+        for (const Mode& md : ms) {
+          const Span sp = mode_span(md);
+          box_r = std::max(box_r, kBackTR + sp.rmax - sp.rmin);
+          box_c = std::max(box_c, kBackTC + sp.cmax - sp.cmin);
+        }
+      box_r = std::max(4, round4(box_r));
+      box_c = std::max(1, box_c);
+    }
+    P.bbox_r = box_r;
+    P.bbox_c = box_c;
+    std::vector<std::vector<uint32_t>> descs;
+    std::vector<int> tiles;
     for (size_t k = 0; k < todo.size(); ++k) {
       const int b0 = todo[k].first, nb = todo[k].second;
-      std::vector<std::vector<TapXY>> cb(bands.begin() + b0, bands.begin() + b0 + nb);
-      std::vector<Mode> ms = cluster_modes(cb);
       std::vector<uint32_t> d;
       int t = 0;
-      if (!back_desc(P, b0, nb, P.back_nb, ms, invh, P.vec_b, d, t)) return fail(CTIS_ERR_TAP, "back window overflow");
+      if (!back_desc(P, b0, nb, P.back_nb, cms[k], invh, box_r, box_c, d, t))
+        return fail(CTIS_ERR_TAP, "back window overflow");
       if ((int)d.size() + kPageHeader > kPageWords) {
         if (nb == 1) return fail(CTIS_ERR_TAP, "band has too many taps for one 64 KB tap page");
-        todo.insert(todo.begin() + (long)k + 1, {b0 + nb / 2, nb - nb / 2});
-        todo[k].second = nb / 2;
+        // split the chunk in two and re-cluster both halves (box stays valid: spans only shrink)
+        const int h = nb / 2;
+        todo.insert(todo.begin() + (long)k + 1, {b0 + h, nb - h});
+        todo[k].second = h;
+        std::vector<std::vector<TapXY>> c1(bands.begin() + b0, bands.begin() + b0 + h);
+        std::vector<std::vector<TapXY>> c2(bands.begin() + b0 + h, bands.begin() + b0 + nb);
+        cms[k] = cluster_modes(c1);
+        cms.insert(cms.begin() + (long)k + 1, cluster_modes(c2));
         --k;
         continue;
       }
       descs.push_back(std::move(d));
       tiles.push_back(t);
-      modes.push_back((int)ms.size());
     }
     std::vector<int> nbs(descs.size(), P.back_nb);  // back pages: "max_modes" carries NB
     pack_pages(P.back, false, descs, tiles, nbs);
   }
   for (Page& pg : P.fwd) {
-    ctis_status st = load_page(pg, P.vec_f);
+    ctis_status st = load_page(pg, P.tma_f);
     if (st) return st;
   }
   for (Page& pg : P.back) {
-    ctis_status st = load_page(pg, P.vec_b);
+    ctis_status st = load_page(pg, P.tma_b);
     if (st) return st;
   }
   return CTIS_OK;
@@ -477,7 +527,8 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
     return fail(CTIS_ERR_DIMENSION, "a, alpha, w, gamma, xi must be >= 1");
   if (gamma < a || xi < alpha) return fail(CTIS_ERR_DIMENSION, "field stop must fit the FPA (gamma >= a, xi >= alpha)");
   const int64_t n = gamma * xi, ell = a * alpha;
-  if (n >= (int64_t(1) << 31) || ell * w >= (int64_t(1) << 31)) return fail(CTIS_ERR_DIMENSION, "n and m must be < 2^31");
+  if (n >= (int64_t(1) << 30) || ell * w >= (int64_t(1) << 31))
+    return fail(CTIS_ERR_DIMENSION, "n must be < 2^30 and m < 2^31");
   if (b0 < 0 || b1 > w || b0 >= b1) return fail(CTIS_ERR_DIMENSION, "band range must be a non-empty subrange of [0, w)");
   if (tap_ptr[0] != 0) return fail(CTIS_ERR_TAP, "tap_ptr[0] must be 0");
   std::vector<float> hband;
@@ -575,15 +626,72 @@ ctis_status check_frames(int64_t frames) {
 }
 
 // ---- launches --------------------------------------------------------------------------------
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link against libcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// f as {a, alpha, w, frames} (forward) or r as {gamma, xi, frames} (back), fp32, zero OOB fill.
+cudaError_t make_tensor_map(CUtensorMap* tm, bool forward, const ctis_plan_s& P, const float* base, int frames) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return cudaErrorNotSupported;
+  CUresult r;
+  if (forward) {
+    const cuuint64_t dims[4] = {(cuuint64_t)P.a, (cuuint64_t)P.alpha, (cuuint64_t)P.w, (cuuint64_t)frames};
+    const cuuint64_t strides[3] = {4ull * P.a, 4ull * P.ell, 4ull * P.m};
+    const cuuint32_t box[4] = {(cuuint32_t)P.fbox_r, (cuuint32_t)P.fbox_c, 1u, 1u};
+    const cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+    r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[3] = {(cuuint64_t)P.gamma, (cuuint64_t)P.xi, (cuuint64_t)frames};
+    const cuuint64_t strides[2] = {4ull * P.gamma, 4ull * P.n};
+    const cuuint32_t box[3] = {(cuuint32_t)P.bbox_r, (cuuint32_t)P.bbox_c, 1u};
+    const cuuint32_t es[3] = {1u, 1u, 1u};
+    r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const float* src, float* dst,
                          long long src_frame, long long dst_frame, int frames, int mode, cudaStream_t s,
                          int64_t* count) {
-  TabArgs A{src, dst, src_frame, dst_frame, P.a, P.alpha, P.gamma, P.n, P.ell, mode};
+  if (pages.empty()) return cudaSuccess;
+  const bool fwd = pages[0].forward;
+  const bool tma = fwd ? P.tma_f : P.tma_b;
+  const long long span = (long long)kModeSpanMax * (P.gamma + 1) + 1;  // max -E(u) over the u-space
+  const unsigned bias = (unsigned)(((span + P.n - 1) / P.n) * P.n);
+  const int box_r = fwd ? P.fbox_r : P.bbox_r, box_c = fwd ? P.fbox_c : P.bbox_c;
+  const int cap = fwd ? kFwdWinFloats : kBackWinFloats;
+  const int slot = tma ? (box_r * box_c + 31) / 32 * 32 : cap;
+  TabArgs A{src, dst, src_frame, dst_frame, P.a, P.alpha, P.gamma, P.xi, P.n, P.ell, mode, bias,
+            slot, box_r, box_c, (unsigned)(4 * box_r * box_c)};
+  alignas(64) CUtensorMap tm;
+  std::memset(&tm, 0, sizeof(tm));
+  if (tma) {
+    cudaError_t e = make_tensor_map(&tm, fwd, P, src, frames);
+    if (e != cudaSuccess) return e;
+  }
+  const int threads = fwd ? kFwdThreads : kBackThreads;
+  const size_t smem = (size_t)kStages * slot * sizeof(float) + 8 * kStages;
   for (const Page& pg : pages) {
     dim3 grid(pg.max_tiles, pg.nchunks, frames);
-    void* args[] = {&A};
-    const int threads = pg.forward ? kFwdThreads : kBackThreads;
-    const size_t smem = kStages * sizeof(float) * (pg.forward ? kFwdWinFloats : kBackWinFloats);
+    void* args[] = {&A, &tm};
     cudaError_t e = cudaLaunchKernel((const void*)pg.kern, grid, dim3(threads), args, smem, s);
     if (e != cudaSuccess) return e;
     if (count) ++*count;

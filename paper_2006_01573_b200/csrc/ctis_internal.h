@@ -56,8 +56,12 @@ struct TabArgs {
   float* dst;          // forward: g_hat (accumulated with red.add); back: f (updated) or z
   long long src_frame; // elements between frames in src
   long long dst_frame; // elements between frames in dst
-  int a, alpha, gamma, n, ell;
+  int a, alpha, gamma, xi, n, ell;
   int mode;            // back: 1 = update f in place, 0 = write z
+  unsigned bias;       // forward: multiple of n with E(u) + bias >= 0 for every u of the u-space
+  int slot_floats;     // floats per pipeline slot (multiple of 32)
+  int box_r, box_c;    // TMA box (window) rows x columns; the window pitch is box_r
+  unsigned box_bytes;  // 4 * box_r * box_c
 };
 
 }  // namespace ctis

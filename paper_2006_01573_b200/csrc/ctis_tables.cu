@@ -14,16 +14,19 @@
 //   wrap of Eq. 7 is reproduced exactly by reducing the final index mod n).
 //
 // forward ("constellation"): a CTA owns a 32 x 16 tile of u = q + (dr, dc) space and ALL
-//   modes of a chunk of bands.  Per band it stages one shared-memory window of f_lam
-//   (cp.async, zero outside the field stop) that every mode reads, accumulates
-//   acc[mode] += w * f_lam[u - (dr, dc)] in registers, and finally adds acc[mode] to
-//   g_hat[(E(u) + o_ref) mod n] with red.global.add.f32 (chunks of bands overlap there).
-// back: a CTA owns a 32 x 32 voxel tile and a chunk of 16 bands; per mode it stages one
-//   shared-memory window of r (1-D modular addressing, exact wrap) that every band of the
-//   chunk reads, accumulates z[band] for 2 voxels per thread in registers, and fuses the
+//   modes of a chunk of bands.  Per band it stages one shared-memory window of f_lam that
+//   every mode reads, accumulates acc[mode] += w * f_lam[u - (dr, dc)] in registers, and
+//   finally adds acc[mode] to g_hat[(E(u) + o_ref) mod n] with red.global.add.f32.
+// back: a CTA owns a 32 x 32 voxel tile and a chunk of NB bands; per mode it stages one
+//   shared-memory window of r (exact 1-D modular addressing) that every band of the chunk
+//   reads, accumulates z[band] for 2 voxels per thread in registers, and fuses the
 //   multiplicative update f <- f * z * (1/h_lam) into the epilogue.
-// Tap metadata (window offsets, weights) is read from __constant__ through the uniform
-// datapath (LDCU + FFMA R,R,UR,R): the only per-FMA shared-memory traffic is the operand.
+// Windows are moved by TMA (cp.async.bulk.tensor, one elected thread, mbarrier completion,
+// zero fill outside the field stop) through a kStages-deep ring; geometries whose strides are
+// not 16-byte multiples (and r windows that wrap around the FPA) use a cp.async element loader.
+// Tap metadata (byte offsets into the window, weights) is read from __constant__ through the
+// uniform datapath (LDCU; LDS [R+UR]; FFMA R,R,UR,R): no per-tap address arithmetic.
+#include <cuda.h>
 #include <stdint.h>
 
 #include "ctis_internal.h"
@@ -34,20 +37,12 @@ __constant__ uint32_t c_tab[kPageWords];
 
 namespace {
 
-__device__ __forceinline__ void cp_async16(float* smem, const float* gmem, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
-}
-
 __device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool valid) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   const int sz = valid ? 4 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
 }
-
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-
 template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
@@ -56,78 +51,89 @@ __device__ __forceinline__ void cp_wait() {
 __device__ __forceinline__ int tabi(uint32_t i) { return (int)c_tab[i]; }
 __device__ __forceinline__ float tabf(uint32_t i) { return __uint_as_float(c_tab[i]); }
 
-// Window loaders.  A window is WR x WC floats (WR <= 64, WR % 4 == 0 on the 16-byte path),
-// stored column by column with pitch WR.  Lanes 0-15 copy 16 four-float chunks of one window
-// column, lanes 16-31 the next column, so a warp covers two columns per pass (32-bit math only).
-
-// f_lam window: element (i, j) = f_lam[(row0 + i) + a*(col0 + j)], zero outside the field stop.
-template <int NWARPS, bool VEC>
-__device__ __forceinline__ void load_f_window(float* buf, const float* fl, const TabArgs& A, int row0, int col0,
-                                              int WR, int WC) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (VEC) {
-    const int i = (lane & 15) * 4, rr = row0 + i;
-    const bool rok = (i < WR) & (rr >= 0) & (rr < A.a);
-    for (int j = 2 * warp + (lane >> 4); j < WC; j += 2 * NWARPS) {
-      const int cc = col0 + j;
-      const bool ok = rok & (cc >= 0) & (cc < A.alpha);
-      if (i < WR) cp_async16(buf + i + WR * j, ok ? fl + rr + A.a * cc : fl, ok);
-    }
-  } else {
-    for (int j = warp; j < WC; j += NWARPS) {
-      const int cc = col0 + j;
-      const bool cok = (cc >= 0) & (cc < A.alpha);
-      for (int i = lane; i < WR; i += 32) {
-        const int rr = row0 + i;
-        const bool ok = cok & (rr >= 0) & (rr < A.a);
-        cp_async4(buf + i + WR * j, ok ? fl + rr + A.a * cc : fl, ok);
-      }
-    }
-  }
-}
-
-// r window: element (i, j) = r[(B + i + gamma*j) mod n]  (0 <= B < n).
-template <int NWARPS, bool VEC>
-__device__ __forceinline__ void load_r_window(float* buf, const float* r, const TabArgs& A, unsigned B, int WR,
-                                              int WC) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned n = (unsigned)A.n;
-  if (VEC) {
-    const int i = (lane & 15) * 4;
-    if (i >= WR) return;
-    const int j0 = 2 * warp + (lane >> 4);
-    unsigned cb = B + (unsigned)A.gamma * (unsigned)j0;
-    while (cb >= n) cb -= n;
-    const unsigned step = (unsigned)A.gamma * (2u * NWARPS);
-    for (int j = j0; j < WC; j += 2 * NWARPS) {
-      unsigned idx = cb + (unsigned)i;
-      while (idx >= n) idx -= n;
-      cp_async16(buf + i + WR * j, r + idx, true);
-      cb += step;
-      while (cb >= n) cb -= n;
-    }
-  } else {
-    for (int j = warp; j < WC; j += NWARPS) {
-      unsigned cb = B + (unsigned)((unsigned long long)A.gamma * (unsigned)j % n);
-      while (cb >= n) cb -= n;
-      for (int i = lane; i < WR; i += 32) {
-        unsigned idx = cb + (unsigned)i;
-        while (idx >= n) idx -= n;
-        cp_async4(buf + i + WR * j, r + idx, true);
-      }
-    }
-  }
-}
-
 __device__ __forceinline__ float lds(unsigned addr) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
 
-template <int MAXM, bool VEC>
-__device__ __forceinline__ void forward_body(const TabArgs& A) {
-  extern __shared__ __align__(16) float smem[];
+// ---- mbarrier / TMA helpers -----------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(unsigned dst, const CUtensorMap* tm, int c0, int c1, int c2, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_4d(unsigned dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3,
+                                       unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(dst),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+
+// ---- element loaders (cp.async, 4 bytes) ----------------------------------------------------
+// f_lam window: element (i, j) = f_lam[(row0 + i) + a*(col0 + j)], zero outside the field stop.
+template <int NWARPS>
+__device__ __forceinline__ void load_f_window(float* buf, const float* fl, const TabArgs& A, int row0, int col0,
+                                              int WR, int WC) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < WC; j += NWARPS) {
+    const int cc = col0 + j;
+    const bool cok = (cc >= 0) & (cc < A.alpha);
+    for (int i = lane; i < WR; i += 32) {
+      const int rr = row0 + i;
+      const bool ok = cok & (rr >= 0) & (rr < A.a);
+      cp_async4(buf + i + WR * j, ok ? fl + rr + A.a * cc : fl, ok);
+    }
+  }
+}
+
+// r window: element (i, j) = r[(B + i + gamma*j) mod n]  (0 <= B < n).
+template <int NWARPS>
+__device__ __forceinline__ void load_r_window(float* buf, const float* r, const TabArgs& A, unsigned B, int WR,
+                                              int WC) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned n = (unsigned)A.n;
+  for (int j = warp; j < WC; j += NWARPS) {
+    unsigned cb = B + (unsigned)((unsigned long long)A.gamma * (unsigned)j % n);
+    while (cb >= n) cb -= n;
+    for (int i = lane; i < WR; i += 32) {
+      unsigned idx = cb + (unsigned)i;
+      while (idx >= n) idx -= n;
+      cp_async4(buf + i + WR * j, r + idx, true);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Forward.  TMA: f viewed as a 4-D tensor {a, alpha, w, frames}; the window box {WRbox, WCbox, 1, 1}
+// starts at (U_r + row0_rel, U_c + col0_rel, lam, frame); out-of-bounds elements are zero.
+template <int MAXM, bool TMA>
+__device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap* tm) {
+  extern __shared__ __align__(128) float smem[];
   const uint32_t D = c_tab[1 + blockIdx.y];
   const int lam0 = tabi(D + 0), nb = tabi(D + 1), nm = tabi(D + 2);
   const int u_r0 = tabi(D + 3), u_c0 = tabi(D + 4), tiles_r = tabi(D + 5), tiles_c = tabi(D + 6);
@@ -138,27 +144,51 @@ __device__ __forceinline__ void forward_body(const TabArgs& A) {
   const float* f = A.src + (long long)blockIdx.z * A.src_frame;
   const uint32_t BI = D + kDescHeader + nm, TP = BI + 4 * nb;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned bars = sbase + kStages * A.slot_floats * 4u;  // kStages mbarriers after the slots
+
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < kStages; ++s) mbar_init(bars + 8 * s, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  auto issue = [&](int b) {
+    const int slot = b % kStages;
+    if (TMA) {
+      if (b < nb && threadIdx.x == 0) {
+        const uint32_t bi = BI + 4 * b;
+        mbar_expect_tx(bars + 8 * slot, A.box_bytes);
+        tma_4d(sbase + 4u * slot * A.slot_floats, tm, U_r + tabi(bi + 0), U_c + tabi(bi + 1), lam0 + b,
+               (int)blockIdx.z, bars + 8 * slot);
+      }
+    } else {
+      if (b < nb) {
+        const uint32_t bi = BI + 4 * b;
+        load_f_window<kFwdThreads / 32>(smem + slot * A.slot_floats, f + (long long)(lam0 + b) * A.ell, A,
+                                        U_r + tabi(bi + 0), U_c + tabi(bi + 1), tabi(bi + 2), tabi(bi + 3));
+      }
+      cp_commit();  // one (possibly empty) group per band keeps the group arithmetic uniform
+    }
+  };
 
   float acc[MAXM];
 #pragma unroll
   for (int c = 0; c < MAXM; ++c) acc[c] = 0.f;
 
-  auto issue = [&](int b) {
-    if (b < nb) {
-      const uint32_t bi = BI + 4 * b;
-      load_f_window<kFwdThreads / 32, VEC>(smem + (b % kStages) * kFwdWinFloats, f + (long long)(lam0 + b) * A.ell, A,
-                                           U_r + tabi(bi + 0), U_c + tabi(bi + 1), tabi(bi + 2), tabi(bi + 3));
-    }
-    cp_commit();  // one (possibly empty) group per band keeps the group arithmetic uniform
-  };
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) issue(s);
   for (int b = 0; b < nb; ++b) {
     issue(b + kStages - 1);
-    cp_wait<kStages - 1>();
-    __syncthreads();
+    const int slot = b % kStages;
+    if (TMA) {
+      mbar_wait(bars + 8 * slot, (unsigned)(b / kStages) & 1u);
+    } else {
+      cp_wait<kStages - 1>();
+      __syncthreads();
+    }
     // byte address of this thread's u in the window; tap entries hold byte offsets (absent: w = 0)
-    const unsigned base = sbase + 4u * ((b % kStages) * kFwdWinFloats + lane + tabi(BI + 4 * b + 2) * warp);
+    const unsigned base = sbase + 4u * (slot * A.slot_floats + lane + tabi(BI + 4 * b + 2) * warp);
     // pointer arithmetic (not an unsigned index) lets ptxas fold 8*c into LDCU.64 c[0x3][UR+imm]
     const uint2* ent = reinterpret_cast<const uint2*>(c_tab + TP) + b * MAXM;
 #pragma unroll
@@ -166,23 +196,32 @@ __device__ __forceinline__ void forward_body(const TabArgs& A) {
       const uint2 e = ent[c];
       acc[c] = fmaf(__uint_as_float(e.y), lds(base + e.x), acc[c]);
     }
-    __syncthreads();
+    __syncthreads();  // every thread is done with this slot before it is refilled
   }
+  // flush: g_hat[(E(u) + o_ref) mod n] += acc.  E(u) = u_r + gamma*u_c can be negative (u reaches
+  // kModeSpanMax outside the field stop); the host-chosen bias (a multiple of n) makes it >= 0, and
+  // the sum stays far below 2^32 (n < 2^30 is enforced at plan creation).
   float* g = A.dst + (long long)blockIdx.z * A.dst_frame;
-  const long long ub = (long long)(U_r + lane) + (long long)A.gamma * (U_c + warp);
+  const unsigned n = (unsigned)A.n;
+  const int ue = (U_r + lane) + A.gamma * (U_c + warp);
+  const unsigned ub = (unsigned)ue + A.bias;
 #pragma unroll
   for (int c = 0; c < MAXM; ++c) {
     if (c < nm && acc[c] != 0.f) {
-      long long P = (ub + tabi(D + kDescHeader + c)) % A.n;
-      if (P < 0) P += A.n;
+      unsigned P = ub + c_tab[D + kDescHeader + c];
+      while (P >= n) P -= n;
       atomicAdd(g + P, acc[c]);
     }
   }
 }
 
-template <int NB, bool VEC>
-__device__ __forceinline__ void back_body(const TabArgs& A) {
-  extern __shared__ __align__(16) float smem[];
+// ------------------------------------------------------------------------------------------------
+// Back.  TMA: r viewed as a 3-D tensor {gamma, xi, frames}; a window whose 1-D origin B = (R0, C0)
+// on the FPA fits without carry/wrap (R0 + WRbox <= gamma, C0 + WCbox <= xi) is one box load; any
+// other window (cyclic wrap of Eq. 7) is loaded element by element with exact modular indices.
+template <int NB, bool TMA>
+__device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* tm) {
+  extern __shared__ __align__(128) float smem[];
   const uint32_t D = c_tab[1 + blockIdx.y];
   const int lam0 = tabi(D + 0), nb = tabi(D + 1), nm = tabi(D + 2);
   const int tiles_r = tabi(D + 3), tiles_c = tabi(D + 4);
@@ -193,31 +232,65 @@ __device__ __forceinline__ void back_body(const TabArgs& A) {
   const float* r = A.src + (long long)blockIdx.z * A.src_frame;
   const uint32_t MI = D + kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * NB;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned bars = sbase + kStages * A.slot_floats * 4u;
   const unsigned tile1d = (unsigned)(q_r0 + A.gamma * q_c0);  // < n
 
-  float acc0[NB], acc1[NB];
-#pragma unroll
-  for (int b = 0; b < NB; ++b) acc0[b] = acc1[b] = 0.f;
-
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < kStages; ++s) mbar_init(bars + 8 * s, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   auto origin = [&](int c) {
     unsigned B = tile1d + c_tab[MI + 4 * c];
     while (B >= (unsigned)A.n) B -= (unsigned)A.n;
     return B;
   };
   auto issue = [&](int c) {
-    if (c < nm)
-      load_r_window<kBackThreads / 32, VEC>(smem + (c % kStages) * kBackWinFloats, r, A, origin(c),
-                                            tabi(MI + 4 * c + 1), tabi(MI + 4 * c + 2));
-    cp_commit();
+    const int slot = c % kStages;
+    if (TMA) {
+      if (c < nm) {
+        const unsigned B = origin(c);
+        const int R0 = (int)(B % (unsigned)A.gamma), C0 = (int)(B / (unsigned)A.gamma);
+        if (R0 + A.box_r <= A.gamma && C0 + A.box_c <= A.xi) {
+          if (threadIdx.x == 0) {
+            mbar_expect_tx(bars + 8 * slot, A.box_bytes);
+            tma_3d(sbase + 4u * slot * A.slot_floats, tm, R0, C0, (int)blockIdx.z, bars + 8 * slot);
+          }
+        } else {  // wrapped window: exact element loads, then complete the slot's phase by hand
+          load_r_window<kBackThreads / 32>(smem + slot * A.slot_floats, r, A, B, A.box_r, A.box_c);
+          cp_commit();
+          cp_wait<0>();
+          __syncthreads();
+          if (threadIdx.x == 0) mbar_arrive(bars + 8 * slot);
+        }
+      }
+    } else {
+      if (c < nm)
+        load_r_window<kBackThreads / 32>(smem + slot * A.slot_floats, r, A, origin(c), tabi(MI + 4 * c + 1),
+                                         tabi(MI + 4 * c + 2));
+      cp_commit();
+    }
   };
+
+  float acc0[NB], acc1[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) acc0[b] = acc1[b] = 0.f;
+
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) issue(s);
   for (int c = 0; c < nm; ++c) {
     issue(c + kStages - 1);
-    cp_wait<kStages - 1>();
-    __syncthreads();
+    const int slot = c % kStages;
+    if (TMA) {
+      mbar_wait(bars + 8 * slot, (unsigned)(c / kStages) & 1u);
+    } else {
+      cp_wait<kStages - 1>();
+      __syncthreads();
+    }
     const int WR = tabi(MI + 4 * c + 1);
-    const unsigned b0a = sbase + 4u * ((c % kStages) * kBackWinFloats + lane + WR * warp);
+    const unsigned b0a = sbase + 4u * (slot * A.slot_floats + lane + WR * warp);
     const unsigned b1a = b0a + 4u * WR * (kBackThreads / 32);
     const uint2* ent = reinterpret_cast<const uint2*>(c_tab + TP) + c * NB;
 #pragma unroll
@@ -251,40 +324,38 @@ __device__ __forceinline__ void back_body(const TabArgs& A) {
 
 }  // namespace
 
-#define CTIS_FWD(M, V, NAME) \
-  extern "C" __global__ void __launch_bounds__(kFwdThreads, 1) NAME(const TabArgs A) { forward_body<M, V>(A); }
-CTIS_FWD(8, true, ctis_fwd_m8_v)
-CTIS_FWD(8, false, ctis_fwd_m8_s)
-CTIS_FWD(16, true, ctis_fwd_m16_v)
-CTIS_FWD(16, false, ctis_fwd_m16_s)
-CTIS_FWD(24, true, ctis_fwd_m24_v)
-CTIS_FWD(24, false, ctis_fwd_m24_s)
-CTIS_FWD(32, true, ctis_fwd_m32_v)
-CTIS_FWD(32, false, ctis_fwd_m32_s)
-CTIS_FWD(40, true, ctis_fwd_m40_v)
-CTIS_FWD(40, false, ctis_fwd_m40_s)
-CTIS_FWD(48, true, ctis_fwd_m48_v)
-CTIS_FWD(48, false, ctis_fwd_m48_s)
-CTIS_FWD(56, true, ctis_fwd_m56_v)
-CTIS_FWD(56, false, ctis_fwd_m56_s)
-CTIS_FWD(64, true, ctis_fwd_m64_v)
-CTIS_FWD(64, false, ctis_fwd_m64_s)
-CTIS_FWD(72, true, ctis_fwd_m72_v)
-CTIS_FWD(72, false, ctis_fwd_m72_s)
-CTIS_FWD(80, true, ctis_fwd_m80_v)
-CTIS_FWD(80, false, ctis_fwd_m80_s)
-CTIS_FWD(88, true, ctis_fwd_m88_v)
-CTIS_FWD(88, false, ctis_fwd_m88_s)
-CTIS_FWD(96, true, ctis_fwd_m96_v)
-CTIS_FWD(96, false, ctis_fwd_m96_s)
+#define CTIS_FWD(M)                                                                                        \
+  extern "C" __global__ void __launch_bounds__(kFwdThreads, 1)                                             \
+      ctis_fwd_m##M##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                         \
+    forward_body<M, true>(A, &tm);                                                                         \
+  }                                                                                                        \
+  extern "C" __global__ void __launch_bounds__(kFwdThreads, 1)                                             \
+      ctis_fwd_m##M##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                         \
+    forward_body<M, false>(A, &tm);                                                                        \
+  }
+CTIS_FWD(8)
+CTIS_FWD(16)
+CTIS_FWD(24)
+CTIS_FWD(32)
+CTIS_FWD(40)
+CTIS_FWD(48)
+CTIS_FWD(56)
+CTIS_FWD(64)
+CTIS_FWD(72)
+CTIS_FWD(80)
+CTIS_FWD(88)
+CTIS_FWD(96)
 
-#define CTIS_BACK(NB, V, NAME) \
-  extern "C" __global__ void __launch_bounds__(kBackThreads, 2) NAME(const TabArgs A) { back_body<NB, V>(A); }
-CTIS_BACK(4, true, ctis_back_b4_v)
-CTIS_BACK(4, false, ctis_back_b4_s)
-CTIS_BACK(8, true, ctis_back_b8_v)
-CTIS_BACK(8, false, ctis_back_b8_s)
-CTIS_BACK(12, true, ctis_back_b12_v)
-CTIS_BACK(12, false, ctis_back_b12_s)
-CTIS_BACK(16, true, ctis_back_b16_v)
-CTIS_BACK(16, false, ctis_back_b16_s)
+#define CTIS_BACK(NB)                                                                                      \
+  extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
+      ctis_back_b##NB##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                       \
+    back_body<NB, true>(A, &tm);                                                                           \
+  }                                                                                                        \
+  extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
+      ctis_back_b##NB##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                       \
+    back_body<NB, false>(A, &tm);                                                                          \
+  }
+CTIS_BACK(4)
+CTIS_BACK(8)
+CTIS_BACK(12)
+CTIS_BACK(16)

@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <cstring>
+static unsigned __float_as_uint_host(float f) { unsigned u; memcpy(&u, &f, 4); return u; }
 
 #define CK(x)                                                                  \
   do {                                                                         \
@@ -114,6 +116,76 @@ __global__ void clock_kernel(long long* out, int spin) {
   }
 }
 
+
+__constant__ uint2 c_taps[4096];
+__device__ __forceinline__ float lds_u(unsigned a) { float v; asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a)); return v; }
+
+// JIT-style tap loop: LDS [R + imm] and FFMA with an immediate weight.
+__global__ void __launch_bounds__(512, 2) taps_imm_kernel(int iters, float* out) {
+  extern __shared__ float s[];
+  for (int i = threadIdx.x; i < 8192; i += blockDim.x) s[i] = (float)i;
+  __syncthreads();
+  const unsigned sb = (unsigned)__cvta_generic_to_shared(s) + 4u * threadIdx.x;
+  float a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = 0.f;
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = fmaf(0.37f + 0.01f * i + 0.1f * k, lds_u(sb + 4u * (37u * i + 301u * k)), a[i]);
+    }
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) t += a[i];
+  if (t == 1.f) out[0] = t;
+}
+
+// Table-style tap loop: (offset, weight) from __constant__ via the uniform datapath.
+__global__ void __launch_bounds__(512, 2) taps_ldcu_kernel(int iters, float* out) {
+  extern __shared__ float s[];
+  for (int i = threadIdx.x; i < 8192; i += blockDim.x) s[i] = (float)i;
+  __syncthreads();
+  const unsigned sb = (unsigned)__cvta_generic_to_shared(s) + 4u * threadIdx.x;
+  float a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = 0.f;
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+    const uint2* e = c_taps + (it & 63) * 64;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint2 t = e[16 * k + i];
+        a[i] = fmaf(__uint_as_float(t.y), lds_u(sb + t.x), a[i]);
+      }
+    }
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) t += a[i];
+  if (t == 1.f) out[0] = t;
+}
+
+// L2-resident streaming read with 8 independent float4 loads in flight per thread.
+__global__ void l2_stream_kernel(const float4* __restrict__ a, int n4, int iters, float* out) {
+  float acc = 0.f;
+  const int stride = gridDim.x * blockDim.x;
+  for (int it = 0; it < iters; ++it) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i + 7 * stride < n4; i += 8 * stride) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(a + i + u * stride);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+    }
+  }
+  if (acc == 123.f) out[0] = acc;
+}
+
 template <typename F>
 float time_ms(F&& f, int reps = 5) {
   cudaEvent_t a, b;
@@ -185,6 +257,26 @@ int main() {
     const double fmas = (double)blocks * threads * it * 16 * 8;
     printf(", \"ffma_per_clk_per_sm\": %.1f, \"fp32_tflops\": %.1f\n", fmas / (ms * 1e-3) / sms / (mhz * 1e6),
            2 * fmas / ms / 1e9);
+  }
+
+  // tap loops (operand delivery with and without table metadata)
+  {
+    std::vector<uint2> h(4096);
+    for (int i = 0; i < 4096; ++i) h[i] = make_uint2(4u * ((i * 37u) % 4096u), __float_as_uint_host(0.5f));
+    CK(cudaMemcpyToSymbol(c_taps, h.data(), sizeof(uint2) * 4096));
+    const int blocks = sms * 2, threads = 512, it = 1 << 12;
+    CK(cudaFuncSetAttribute(taps_imm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
+    ms = time_ms([&] { taps_imm_kernel<<<blocks, threads, 40 * 1024>>>(it, out); });
+    double fmas = (double)blocks * threads * it * 64;
+    printf(", \"taps_imm_fma_per_clk_per_sm\": %.2f\n", fmas / (ms * 1e-3) / sms / (mhz * 1e6));
+    ms = time_ms([&] { taps_ldcu_kernel<<<blocks, threads, 40 * 1024>>>(it, out); });
+    printf(", \"taps_ldcu_fma_per_clk_per_sm\": %.2f\n", fmas / (ms * 1e-3) / sms / (mhz * 1e6));
+  }
+  // L2 streaming read (64 MB buffer, resident)
+  {
+    const int n4 = (64 << 20) / 16;
+    ms = time_ms([&] { l2_stream_kernel<<<sms * 4, 512>>>((const float4*)A, n4, 8, out); });
+    printf(", \"l2_stream_read_gbs\": %.1f\n", 8.0 * n4 * 16 / ms / 1e6);
   }
   // reductions into a 16 MB L2-resident buffer
   {
