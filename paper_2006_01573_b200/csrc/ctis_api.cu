@@ -253,18 +253,21 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
   out[7] = (uint32_t)maxm;
   for (int c = 0; c < nm; ++c) out[kDescHeader + c] = (uint32_t)(ms[c]->ref_dr + P.gamma * ms[c]->ref_dc);
   const int BI = kDescHeader + nm, TP = BI + 4 * nb;
-  std::vector<int> WRs(nb, 1);
+  std::vector<int> WRs(nb, 1), lead(nb, 0);
   for (int b = 0; b < nb; ++b) {
     if (sp[b].empty()) {  // band without taps in this pass: any window, never read
       out[BI + 4 * b + 2] = (uint32_t)std::max(box_r, 1);
       out[BI + 4 * b + 3] = box_r ? (uint32_t)box_c : 0u;
       continue;
     }
+    // TMA: the innermost box coordinate must be a multiple of 4 floats (16 bytes); the tile row
+    // origin is all.rmin + 32*k, so start the window `lead` rows early.
+    lead[b] = box_r ? (int)((((long long)all.rmin - sp[b].rmax) % 4 + 4) % 4) : 0;
     const int WR = box_r ? box_r : kFwdTR + sp[b].rmax - sp[b].rmin;
     const int WC = box_r ? box_c : kFwdTC + sp[b].cmax - sp[b].cmin;
-    if (WR * WC > kFwdWinFloats) return false;
+    if (WR * WC > kFwdWinFloats || (box_r && kFwdTR + sp[b].rmax - sp[b].rmin + lead[b] > box_r)) return false;
     WRs[b] = WR;
-    out[BI + 4 * b + 0] = (uint32_t)(-sp[b].rmax);
+    out[BI + 4 * b + 0] = (uint32_t)(-sp[b].rmax - lead[b]);
     out[BI + 4 * b + 1] = (uint32_t)(-sp[b].cmax);
     out[BI + 4 * b + 2] = (uint32_t)WR;
     out[BI + 4 * b + 3] = (uint32_t)WC;
@@ -272,7 +275,7 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
   for (int c = 0; c < nm; ++c)
     for (const ModeTap& t : ms[c]->taps) {
       const int dr = t.dr - ms[c]->ref_dr, dc = t.dc - ms[c]->ref_dc;
-      const int off = (sp[t.b].rmax - dr) + WRs[t.b] * (sp[t.b].cmax - dc);
+      const int off = (sp[t.b].rmax + lead[t.b] - dr) + WRs[t.b] * (sp[t.b].cmax - dc);
       out[TP + 2 * (t.b * maxm + c)] = (uint32_t)(4 * off);
       out[TP + 2 * (t.b * maxm + c) + 1] = fbits(t.w);
     }
@@ -297,17 +300,21 @@ bool back_desc(const ctis_plan_s& P, int b0, int nb, int NB, const std::vector<M
     const Mode& md = ms[c];
     const Span sp = mode_span(md);
     const long long oref = (long long)md.ref_dr + (long long)P.gamma * md.ref_dc;
-    long long Bm = (oref + sp.rmin + (long long)P.gamma * sp.cmin) % P.n;
+    const long long B0 = oref + sp.rmin + (long long)P.gamma * sp.cmin;
+    // TMA: the window's FPA row origin (B mod gamma; gamma % 4 == 0 and tile origins are multiples
+    // of 32) must be a multiple of 4, so start `lead` rows early.
+    const int lead = box_r ? (int)(((B0 % 4) + 4) % 4) : 0;
+    long long Bm = (B0 - lead) % P.n;
     if (Bm < 0) Bm += P.n;
     const int WR = box_r ? box_r : kBackTR + sp.rmax - sp.rmin;
     const int WC = box_r ? box_c : kBackTC + sp.cmax - sp.cmin;
-    if (WR * WC > kBackWinFloats) return false;
+    if (WR * WC > kBackWinFloats || (box_r && kBackTR + sp.rmax - sp.rmin + lead > box_r)) return false;
     out[MI + 4 * c + 0] = (uint32_t)Bm;
     out[MI + 4 * c + 1] = (uint32_t)WR;
     out[MI + 4 * c + 2] = (uint32_t)WC;
     for (const ModeTap& t : md.taps) {
       const int dr = t.dr - md.ref_dr, dc = t.dc - md.ref_dc;
-      out[TP + 2 * (c * NB + t.b)] = (uint32_t)(4 * ((dr - sp.rmin) + WR * (dc - sp.cmin)));
+      out[TP + 2 * (c * NB + t.b)] = (uint32_t)(4 * ((dr - sp.rmin + lead) + WR * (dc - sp.cmin)));
       out[TP + 2 * (c * NB + t.b) + 1] = fbits(t.w);
     }
   }
@@ -433,7 +440,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
       for (size_t i = 0; i < passes.size(); ++i)
         for (const Span& x : band_spans(chunks[pass_chunk[i]].second, passes[i]))
           if (!x.empty()) {
-            box_r = std::max(box_r, kFwdTR + x.rmax - x.rmin);
+            box_r = std::max(box_r, kFwdTR + x.rmax - x.rmin + 3);
             box_c = std::max(box_c, kFwdTC + x.cmax - x.cmin);
           }
       box_r = std::max(4, round4(box_r));
@@ -471,7 +478,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
       for (const auto& ms : cms)
         for (const Mode& md : ms) {
           const Span sp = mode_span(md);
-          box_r = std::max(box_r, kBackTR + sp.rmax - sp.rmin);
+          box_r = std::max(box_r, kBackTR + sp.rmax - sp.rmin + 3);
           box_c = std::max(box_c, kBackTC + sp.cmax - sp.cmin);
         }
       box_r = std::max(4, round4(box_r));

@@ -47,8 +47,8 @@ constexpr int kBackBandsMax = 16;
 // never exceeds (32 + 24 + 3 -> 60) x (16 + 24) floats (forward) or 60 x (32 + 24) (back).
 constexpr int kModeSpanMax = 12;
 constexpr int kStages = 3;              // window pipeline depth (cp.async groups in flight)
-constexpr int kFwdWinFloats = 2560;     // 10 KB per stage
-constexpr int kBackWinFloats = 3584;    // 14 KB per stage
+constexpr int kFwdWinFloats = 2560;     // 10 KB per stage (>= 60 x 40)
+constexpr int kBackWinFloats = 3584;    // 14 KB per stage (>= 60 x 56)
 
 // Per-launch parameters of the table kernels.
 struct TabArgs {
