@@ -242,7 +242,8 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
   if (all.empty()) return true;  // no taps: nothing to emit
   const int tiles_r = (P.a + all.rmax - all.rmin + kFwdTR - 1) / kFwdTR;
   const int tiles_c = (P.alpha + all.cmax - all.cmin + kFwdTC - 1) / kFwdTC;
-  out.assign(kDescHeader + nm + 4 * nb + 2 * nb * maxm, 0u);
+  const int nm2 = (nm + 1) & ~1;  // keeps the tap entries at even word offsets (one LDCU.64 each)
+  out.assign(kDescHeader + nm2 + 4 * nb + 2 * nb * maxm, 0u);
   out[0] = (uint32_t)b0;
   out[1] = (uint32_t)nb;
   out[2] = (uint32_t)nm;
@@ -252,7 +253,7 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
   out[6] = (uint32_t)tiles_c;
   out[7] = (uint32_t)maxm;
   for (int c = 0; c < nm; ++c) out[kDescHeader + c] = (uint32_t)(ms[c]->ref_dr + P.gamma * ms[c]->ref_dc);
-  const int BI = kDescHeader + nm, TP = BI + 4 * nb;
+  const int BI = kDescHeader + nm2, TP = BI + 4 * nb;
   std::vector<int> WRs(nb, 1), lead(nb, 0);
   for (int b = 0; b < nb; ++b) {
     if (sp[b].empty()) {  // band without taps in this pass: any window, never read
@@ -287,7 +288,7 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
 bool back_desc(const ctis_plan_s& P, int b0, int nb, int NB, const std::vector<Mode>& ms,
                const std::vector<float>& invh, int box_r, int box_c, std::vector<uint32_t>& out, int& tiles) {
   const int nm = (int)ms.size();
-  out.assign(kDescHeader + 4 * nm + 2 * nm * NB + nb, 0u);
+  out.assign(kDescHeader + 4 * nm + 2 * nm * NB + ((nb + 1) & ~1), 0u);  // even length
   const int tiles_r = (P.a + kBackTR - 1) / kBackTR, tiles_c = (P.alpha + kBackTC - 1) / kBackTC;
   out[0] = (uint32_t)b0;
   out[1] = (uint32_t)nb;

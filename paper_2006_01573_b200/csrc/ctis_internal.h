@@ -14,14 +14,14 @@ namespace ctis {
 // datapath (LDCU -> FFMA R, R, UR, R): tap metadata costs no L1/SMEM bandwidth.
 constexpr int kPageWords = 16384;  // 64 KB of uint32
 
-// Page layout (uint32 words):
+// Page layout (uint32 words; every descriptor starts and its tap entries sit at even offsets):
 //   [0]       number of chunks in the page
 //   [1 + k]   word offset of chunk k's descriptor
 //
 // Forward chunk descriptor (Eq. 12 evaluated per "mode"):
 //   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] u_r0   [D+4] u_c0   [D+5] tiles_r   [D+6] tiles_c  [D+7] MAXM
-//   [D+8 ..]            o_ref[c]                     (nm words, 1-D reference offset in [0, n))
-//   [BI = D+8+nm ..]    per band b: row0_rel, col0_rel, WR, WC   (window rows/cols relative to the tile)
+//   [D+8 ..]            o_ref[c]                     (nm words rounded up to even, in [0, n))
+//   [BI = D+8+nm2 ..]   per band b: row0_rel, col0_rel, WR, WC   (window rows/cols relative to the tile)
 //   [TP = BI+4*nb ..]   per (b, c), c < MAXM: byte offset, w-bits  (index TP + 2*(b*MAXM + c);
 //                       w = 0 -> no tap; MAXM = nm rounded up to 8 = the kernel template)
 // Back chunk descriptor (Eqs. 14-15):

@@ -33,7 +33,11 @@
 
 using namespace ctis;
 
-__constant__ uint32_t c_tab[kPageWords];
+// 16-byte aligned so that tap entries (uint2 at even word offsets) load as one LDCU.64
+__constant__ __align__(16) uint32_t c_tab[kPageWords];
+__device__ __forceinline__ const uint2* tab2(uint32_t even_word) {
+  return reinterpret_cast<const uint2*>(c_tab) + (even_word >> 1);
+}
 
 namespace {
 
@@ -142,7 +146,7 @@ __device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int U_r = u_r0 + (tile % tiles_r) * kFwdTR, U_c = u_c0 + (tile / tiles_r) * kFwdTC;
   const float* f = A.src + (long long)blockIdx.z * A.src_frame;
-  const uint32_t BI = D + kDescHeader + nm, TP = BI + 4 * nb;
+  const uint32_t BI = D + kDescHeader + ((nm + 1) & ~1), TP = BI + 4 * nb;  // all even
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
   const unsigned bars = sbase + kStages * A.slot_floats * 4u;  // kStages mbarriers after the slots
 
@@ -190,7 +194,7 @@ __device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap
     // byte address of this thread's u in the window; tap entries hold byte offsets (absent: w = 0)
     const unsigned base = sbase + 4u * (slot * A.slot_floats + lane + tabi(BI + 4 * b + 2) * warp);
     // pointer arithmetic (not an unsigned index) lets ptxas fold 8*c into LDCU.64 c[0x3][UR+imm]
-    const uint2* ent = reinterpret_cast<const uint2*>(c_tab + TP) + b * MAXM;
+    const uint2* ent = tab2(TP) + b * MAXM;
 #pragma unroll
     for (int c = 0; c < MAXM; ++c) {
       const uint2 e = ent[c];
@@ -292,7 +296,7 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
     const int WR = tabi(MI + 4 * c + 1);
     const unsigned b0a = sbase + 4u * (slot * A.slot_floats + lane + WR * warp);
     const unsigned b1a = b0a + 4u * WR * (kBackThreads / 32);
-    const uint2* ent = reinterpret_cast<const uint2*>(c_tab + TP) + c * NB;
+    const uint2* ent = tab2(TP) + c * NB;
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const uint2 e = ent[b];
