@@ -88,6 +88,7 @@ struct ctis_plan_s {
   bool tma_f = false, tma_b = false;
   int back_nb = kBackBandsMax;
   int fbox_r = 0, fbox_c = 0, bbox_r = 0, bbox_c = 0;
+  int fwd_g = 1, fwd_m = 8;
   std::vector<Page> fwd, back;
   float* d_hband = nullptr;
   int* d_flag = nullptr;
@@ -310,9 +311,10 @@ bool back_desc(const ctis_plan_s& P, int b0, int nb, int NB, const std::vector<M
     const int WR = box_r ? box_r : kBackTR + sp.rmax - sp.rmin;
     const int WC = box_r ? box_c : kBackTC + sp.cmax - sp.cmin;
     if (WR * WC > kBackWinFloats || (box_r && kBackTR + sp.rmax - sp.rmin + lead > box_r)) return false;
-    out[MI + 4 * c + 0] = (uint32_t)Bm;
-    out[MI + 4 * c + 1] = (uint32_t)WR;
-    out[MI + 4 * c + 2] = (uint32_t)WC;
+    out[MI + 4 * c + 0] = (uint32_t)(Bm % P.gamma);
+    out[MI + 4 * c + 1] = (uint32_t)(Bm / P.gamma);
+    out[MI + 4 * c + 2] = (uint32_t)WR;
+    out[MI + 4 * c + 3] = (uint32_t)WC;
     for (const ModeTap& t : md.taps) {
       const int dr = t.dr - md.ref_dr, dc = t.dc - md.ref_dc;
       out[TP + 2 * (c * NB + t.b)] = (uint32_t)(4 * ((dr - sp.rmin + lead) + WR * (dc - sp.cmin)));
@@ -372,7 +374,8 @@ ctis_status load_page(Page& pg, bool vec) {
   CTIS_CUDA(cudaMemcpy(dptr, pg.words.data(), pg.words.size() * 4, cudaMemcpyHostToDevice), "upload tap page");
   std::string name;
   if (pg.forward) {
-    name = "ctis_fwd_m" + std::to_string(pg.max_modes) + (vec ? "_t" : "_s");
+    name = "ctis_fwd_g" + std::to_string(pg.max_modes / 1000) + "_m" + std::to_string(pg.max_modes % 1000) +
+           (vec ? "_t" : "_s");
   } else {
     name = "ctis_back_b" + std::to_string(pg.max_modes) + (vec ? "_t" : "_s");
   }
@@ -421,12 +424,22 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
   {
     std::vector<std::vector<Mode>> chunk_modes;
     std::vector<std::pair<int, int>> chunks = balanced_chunks(P.w, kFwdBands);
-    int maxm = 8;
+    int nm_max = 1;
     for (auto [b0, nb] : chunks) {
       std::vector<std::vector<TapXY>> cb(bands.begin() + b0, bands.begin() + b0 + nb);
       chunk_modes.push_back(cluster_modes(cb));
-      maxm = std::max(maxm, std::min(96, ((int)chunk_modes.back().size() + 7) / 8 * 8));
+      nm_max = std::max(nm_max, (int)chunk_modes.back().size());
     }
+    // <= 64 modes: two 16-warp groups split the modes (MAXM per group, multiple of 4, <= 32, keeps
+    // the 1024-thread CTA within 64 registers); otherwise one group with up to 96 modes per pass.
+    if (nm_max <= 64) {
+      P.fwd_g = 2;
+      P.fwd_m = std::max(4, ((nm_max + 1) / 2 + 3) / 4 * 4);
+    } else {
+      P.fwd_g = 1;
+      P.fwd_m = std::min(96, (nm_max + 7) / 8 * 8);
+    }
+    const int maxm = P.fwd_g * P.fwd_m;  // modes per pass
     std::vector<std::vector<const Mode*>> passes;
     std::vector<int> pass_chunk;
     for (size_t k = 0; k < chunk_modes.size(); ++k)
@@ -460,7 +473,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
       if (d.empty()) continue;
       descs.push_back(std::move(d));
       tiles.push_back(t);
-      modes.push_back(maxm);
+      modes.push_back(1000 * P.fwd_g + P.fwd_m);  // forward pages: "max_modes" encodes the template
     }
     pack_pages(P.fwd, true, descs, tiles, modes);
   }
@@ -683,11 +696,15 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
   const bool fwd = pages[0].forward;
   const bool tma = fwd ? P.tma_f : P.tma_b;
   const long long span = (long long)kModeSpanMax * (P.gamma + 1) + 1;  // max -E(u) over the u-space
-  const unsigned bias = (unsigned)(((span + P.n - 1) / P.n) * P.n);
+  const long long kb = (span + P.n - 1) / P.n;
+  const unsigned bias = (unsigned)(kb * P.n);
+  // E(u) <= (a + kModeSpanMax) + gamma*(alpha + kModeSpanMax) < 2n (field stop fits the FPA), o_ref < n
+  const long long emax = (long long)(P.a + kModeSpanMax) + (long long)P.gamma * (P.alpha + kModeSpanMax);
+  const int nsub = (int)((bias + emax + P.n - 1) / P.n);
   const int box_r = fwd ? P.fbox_r : P.bbox_r, box_c = fwd ? P.fbox_c : P.bbox_c;
   const int cap = fwd ? kFwdWinFloats : kBackWinFloats;
   const int slot = tma ? (box_r * box_c + 31) / 32 * 32 : cap;
-  TabArgs A{src, dst, src_frame, dst_frame, P.a, P.alpha, P.gamma, P.xi, P.n, P.ell, mode, bias,
+  TabArgs A{src, dst, src_frame, dst_frame, P.a, P.alpha, P.gamma, P.xi, P.n, P.ell, mode, bias, nsub,
             slot, box_r, box_c, (unsigned)(4 * box_r * box_c)};
   alignas(64) CUtensorMap tm;
   std::memset(&tm, 0, sizeof(tm));
@@ -695,7 +712,7 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
     cudaError_t e = make_tensor_map(&tm, fwd, P, src, frames);
     if (e != cudaSuccess) return e;
   }
-  const int threads = fwd ? kFwdThreads : kBackThreads;
+  const int threads = fwd ? P.fwd_g * kFwdThreads : kBackThreads;
   const size_t smem = (size_t)kStages * slot * sizeof(float) + 8 * kStages;
   for (const Page& pg : pages) {
     dim3 grid(pg.max_tiles, pg.nchunks, frames);

@@ -19,22 +19,23 @@ constexpr int kPageWords = 16384;  // 64 KB of uint32
 //   [1 + k]   word offset of chunk k's descriptor
 //
 // Forward chunk descriptor (Eq. 12 evaluated per "mode"):
-//   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] u_r0   [D+4] u_c0   [D+5] tiles_r   [D+6] tiles_c  [D+7] MAXM
+//   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] u_r0   [D+4] u_c0   [D+5] tiles_r   [D+6] tiles_c  [D+7] G*MAXM
 //   [D+8 ..]            o_ref[c]                     (nm words rounded up to even, in [0, n))
 //   [BI = D+8+nm2 ..]   per band b: row0_rel, col0_rel, WR, WC   (window rows/cols relative to the tile)
-//   [TP = BI+4*nb ..]   per (b, c), c < MAXM: byte offset, w-bits  (index TP + 2*(b*MAXM + c);
-//                       w = 0 -> no tap; MAXM = nm rounded up to 8 = the kernel template)
+//   [TP = BI+4*nb ..]   per (b, g, c), c < MAXM: byte offset, w-bits (index TP + 2*((b*G + g)*MAXM + c));
+//                       mode = g*MAXM + c; w = 0 -> no tap; G, MAXM = the kernel template
 // Back chunk descriptor (Eqs. 14-15):
 //   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] tiles_r   [D+4] tiles_c   [D+5] NB   [D+6..7] 0
-//   [MI = D+8 ..]       per mode c: Bm, WR, WC, 0    (window origin term in [0, n))
+//   [MI = D+8 ..]       per mode c: Bm_r, Bm_c, WR, WC  (window origin term Bm = Bm_r + gamma*Bm_c in [0, n))
 //   [TP = MI+4*nm ..]   per (c, b), b < NB: byte offset, w-bits  (index TP + 2*(c*NB + b))
 //   [IH = TP+2*nm*NB ..] inv_h[b]
 enum : int { kDescHeader = 8 };
 
-// Forward kernel geometry: one u-space position per thread, 32 rows x 16 columns per CTA.
+// Forward kernel geometry: one u-space position per thread, 32 rows x 16 columns per CTA; a CTA
+// has G in {1, 2} groups of kFwdThreads threads that share each window and split the modes.
 constexpr int kFwdTR = 32;
 constexpr int kFwdTC = 16;
-constexpr int kFwdThreads = kFwdTR * kFwdTC;
+constexpr int kFwdThreads = kFwdTR * kFwdTC;   // per group
 constexpr int kFwdBands = 16;           // max bands per forward chunk (chunks are balanced)
 // Back kernel geometry: 32 x 32 voxel tile, 2 voxels per thread, NB in {4, 8, 12, 16} bands
 // per chunk (kernel template; the plan picks the one that fills the 148 SMs best).
@@ -59,6 +60,7 @@ struct TabArgs {
   int a, alpha, gamma, xi, n, ell;
   int mode;            // back: 1 = update f in place, 0 = write z
   unsigned bias;       // forward: multiple of n with E(u) + bias >= 0 for every u of the u-space
+  int nsub;            // forward: E(u) + bias + o_ref < (nsub + 1) * n
   int slot_floats;     // floats per pipeline slot (multiple of 32)
   int box_r, box_c;    // TMA box (window) rows x columns; the window pitch is box_r
   unsigned box_bytes;  // 4 * box_r * box_c

@@ -135,7 +135,8 @@ __device__ __forceinline__ void load_r_window(float* buf, const float* r, const 
 // ------------------------------------------------------------------------------------------------
 // Forward.  TMA: f viewed as a 4-D tensor {a, alpha, w, frames}; the window box {WRbox, WCbox, 1, 1}
 // starts at (U_r + row0_rel, U_c + col0_rel, lam, frame); out-of-bounds elements are zero.
-template <int MAXM, bool TMA>
+// G groups of 16 warps share every window; group g owns modes [g*MAXM, (g+1)*MAXM) of the pass.
+template <int G, int MAXM, bool TMA>
 __device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap* tm) {
   extern __shared__ __align__(128) float smem[];
   const uint32_t D = c_tab[1 + blockIdx.y];
@@ -143,7 +144,7 @@ __device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap
   const int u_r0 = tabi(D + 3), u_c0 = tabi(D + 4), tiles_r = tabi(D + 5), tiles_c = tabi(D + 6);
   const int tile = blockIdx.x;
   if (tile >= tiles_r * tiles_c) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) & 15, grp = threadIdx.x >> 9;
   const int U_r = u_r0 + (tile % tiles_r) * kFwdTR, U_c = u_c0 + (tile / tiles_r) * kFwdTC;
   const float* f = A.src + (long long)blockIdx.z * A.src_frame;
   const uint32_t BI = D + kDescHeader + ((nm + 1) & ~1), TP = BI + 4 * nb;  // all even
@@ -169,7 +170,7 @@ __device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap
     } else {
       if (b < nb) {
         const uint32_t bi = BI + 4 * b;
-        load_f_window<kFwdThreads / 32>(smem + slot * A.slot_floats, f + (long long)(lam0 + b) * A.ell, A,
+        load_f_window<G * kFwdThreads / 32>(smem + slot * A.slot_floats, f + (long long)(lam0 + b) * A.ell, A,
                                         U_r + tabi(bi + 0), U_c + tabi(bi + 1), tabi(bi + 2), tabi(bi + 3));
       }
       cp_commit();  // one (possibly empty) group per band keeps the group arithmetic uniform
@@ -194,7 +195,7 @@ __device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap
     // byte address of this thread's u in the window; tap entries hold byte offsets (absent: w = 0)
     const unsigned base = sbase + 4u * (slot * A.slot_floats + lane + tabi(BI + 4 * b + 2) * warp);
     // pointer arithmetic (not an unsigned index) lets ptxas fold 8*c into LDCU.64 c[0x3][UR+imm]
-    const uint2* ent = tab2(TP) + b * MAXM;
+    const uint2* ent = tab2(TP) + (b * G + grp) * MAXM;
 #pragma unroll
     for (int c = 0; c < MAXM; ++c) {
       const uint2 e = ent[c];
@@ -211,9 +212,9 @@ __device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap
   const unsigned ub = (unsigned)ue + A.bias;
 #pragma unroll
   for (int c = 0; c < MAXM; ++c) {
-    if (c < nm && acc[c] != 0.f) {
-      unsigned P = ub + c_tab[D + kDescHeader + c];
-      while (P >= n) P -= n;
+    if (grp * MAXM + c < nm && acc[c] != 0.f) {
+      unsigned P = ub + c_tab[D + kDescHeader + grp * MAXM + c];  // < (nsub + 1) * n
+      for (int k = 0; k < A.nsub; ++k) P = min(P, P - n);  // unsigned: subtracts n iff P >= n
       atomicAdd(g + P, acc[c]);
     }
   }
@@ -237,7 +238,6 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
   const uint32_t MI = D + kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * NB;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
   const unsigned bars = sbase + kStages * A.slot_floats * 4u;
-  const unsigned tile1d = (unsigned)(q_r0 + A.gamma * q_c0);  // < n
 
   if (TMA) {
     if (threadIdx.x == 0) {
@@ -246,36 +246,40 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
     }
     __syncthreads();
   }
-  auto origin = [&](int c) {
-    unsigned B = tile1d + c_tab[MI + 4 * c];
-    while (B >= (unsigned)A.n) B -= (unsigned)A.n;
-    return B;
+  // Window origin on the FPA: B = (tile1d + Bm) mod n as (R0, C0), from the host-split
+  // Bm = Bm_r + gamma*Bm_c with one carry and one wrap (no division).
+  auto origin_rc = [&](int c, int& R0, int& C0) {
+    R0 = q_r0 + tabi(MI + 4 * c + 0);
+    C0 = q_c0 + tabi(MI + 4 * c + 1);
+    if (R0 >= A.gamma) {
+      R0 -= A.gamma;
+      C0 += 1;
+    }
+    if (C0 >= A.xi) C0 -= A.xi;
   };
   auto issue = [&](int c) {
     const int slot = c % kStages;
-    if (TMA) {
-      if (c < nm) {
-        const unsigned B = origin(c);
-        const int R0 = (int)(B % (unsigned)A.gamma), C0 = (int)(B / (unsigned)A.gamma);
-        if (R0 + A.box_r <= A.gamma && C0 + A.box_c <= A.xi) {
-          if (threadIdx.x == 0) {
-            mbar_expect_tx(bars + 8 * slot, A.box_bytes);
-            tma_3d(sbase + 4u * slot * A.slot_floats, tm, R0, C0, (int)blockIdx.z, bars + 8 * slot);
-          }
-        } else {  // wrapped window: exact element loads, then complete the slot's phase by hand
-          load_r_window<kBackThreads / 32>(smem + slot * A.slot_floats, r, A, B, A.box_r, A.box_c);
+    if (c < nm) {
+      int R0, C0;
+      origin_rc(c, R0, C0);
+      if (TMA && R0 + A.box_r <= A.gamma && C0 + A.box_c <= A.xi) {
+        if (threadIdx.x == 0) {
+          mbar_expect_tx(bars + 8 * slot, A.box_bytes);
+          tma_3d(sbase + 4u * slot * A.slot_floats, tm, R0, C0, (int)blockIdx.z, bars + 8 * slot);
+        }
+      } else {  // element loads with exact modular indices (wrapped windows, unaligned geometries)
+        const unsigned B = (unsigned)R0 + (unsigned)A.gamma * (unsigned)C0;
+        const int WR = TMA ? A.box_r : tabi(MI + 4 * c + 2), WC = TMA ? A.box_c : tabi(MI + 4 * c + 3);
+        load_r_window<kBackThreads / 32>(smem + slot * A.slot_floats, r, A, B, WR, WC);
+        if (TMA) {  // complete the slot's phase by hand
           cp_commit();
           cp_wait<0>();
           __syncthreads();
           if (threadIdx.x == 0) mbar_arrive(bars + 8 * slot);
         }
       }
-    } else {
-      if (c < nm)
-        load_r_window<kBackThreads / 32>(smem + slot * A.slot_floats, r, A, origin(c), tabi(MI + 4 * c + 1),
-                                         tabi(MI + 4 * c + 2));
-      cp_commit();
     }
+    if (!TMA) cp_commit();
   };
 
   float acc0[NB], acc1[NB];
@@ -293,7 +297,7 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
       cp_wait<kStages - 1>();
       __syncthreads();
     }
-    const int WR = tabi(MI + 4 * c + 1);
+    const int WR = tabi(MI + 4 * c + 2);
     const unsigned b0a = sbase + 4u * (slot * A.slot_floats + lane + WR * warp);
     const unsigned b1a = b0a + 4u * WR * (kBackThreads / 32);
     const uint2* ent = tab2(TP) + c * NB;
@@ -328,27 +332,35 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
 
 }  // namespace
 
-#define CTIS_FWD(M)                                                                                        \
-  extern "C" __global__ void __launch_bounds__(kFwdThreads, 1)                                             \
-      ctis_fwd_m##M##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                         \
-    forward_body<M, true>(A, &tm);                                                                         \
+#define CTIS_FWD(G, M)                                                                                     \
+  extern "C" __global__ void __launch_bounds__(G * kFwdThreads, 1)                                         \
+      ctis_fwd_g##G##_m##M##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                  \
+    forward_body<G, M, true>(A, &tm);                                                                      \
   }                                                                                                        \
-  extern "C" __global__ void __launch_bounds__(kFwdThreads, 1)                                             \
-      ctis_fwd_m##M##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                         \
-    forward_body<M, false>(A, &tm);                                                                        \
+  extern "C" __global__ void __launch_bounds__(G * kFwdThreads, 1)                                         \
+      ctis_fwd_g##G##_m##M##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                  \
+    forward_body<G, M, false>(A, &tm);                                                                     \
   }
-CTIS_FWD(8)
-CTIS_FWD(16)
-CTIS_FWD(24)
-CTIS_FWD(32)
-CTIS_FWD(40)
-CTIS_FWD(48)
-CTIS_FWD(56)
-CTIS_FWD(64)
-CTIS_FWD(72)
-CTIS_FWD(80)
-CTIS_FWD(88)
-CTIS_FWD(96)
+CTIS_FWD(2, 4)
+CTIS_FWD(2, 8)
+CTIS_FWD(2, 12)
+CTIS_FWD(2, 16)
+CTIS_FWD(2, 20)
+CTIS_FWD(2, 24)
+CTIS_FWD(2, 28)
+CTIS_FWD(2, 32)
+CTIS_FWD(1, 8)
+CTIS_FWD(1, 16)
+CTIS_FWD(1, 24)
+CTIS_FWD(1, 32)
+CTIS_FWD(1, 40)
+CTIS_FWD(1, 48)
+CTIS_FWD(1, 56)
+CTIS_FWD(1, 64)
+CTIS_FWD(1, 72)
+CTIS_FWD(1, 80)
+CTIS_FWD(1, 88)
+CTIS_FWD(1, 96)
 
 #define CTIS_BACK(NB)                                                                                      \
   extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
