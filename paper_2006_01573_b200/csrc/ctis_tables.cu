@@ -135,16 +135,19 @@ __device__ __forceinline__ void load_r_window(float* buf, const float* r, const 
 // ------------------------------------------------------------------------------------------------
 // Forward.  TMA: f viewed as a 4-D tensor {a, alpha, w, frames}; the window box {WRbox, WCbox, 1, 1}
 // starts at (U_r + row0_rel, U_c + col0_rel, lam, frame); out-of-bounds elements are zero.
-// G groups of 16 warps share every window; group g owns modes [g*MAXM, (g+1)*MAXM) of the pass.
-template <int G, int MAXM, bool TMA>
-__device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap* tm) {
+// G groups of 16 warps share every window; group GRP owns modes [GRP*MAXM, (GRP+1)*MAXM) of the
+// pass.  GRP is a template parameter (dispatched on a warp-uniform branch) so that the tap-table
+// pointer stays uniform and the entries load through LDCU.64 rather than per-thread LDC.
+template <int G, int MAXM, bool TMA, int GRP>
+__device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMap* tm) {
   extern __shared__ __align__(128) float smem[];
   const uint32_t D = c_tab[1 + blockIdx.y];
   const int lam0 = tabi(D + 0), nb = tabi(D + 1), nm = tabi(D + 2);
   const int u_r0 = tabi(D + 3), u_c0 = tabi(D + 4), tiles_r = tabi(D + 5), tiles_c = tabi(D + 6);
   const int tile = blockIdx.x;
   if (tile >= tiles_r * tiles_c) return;
-  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) & 15, grp = threadIdx.x >> 9;
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) & 15;
+  constexpr int grp = GRP;
   const int U_r = u_r0 + (tile % tiles_r) * kFwdTR, U_c = u_c0 + (tile / tiles_r) * kFwdTC;
   const float* f = A.src + (long long)blockIdx.z * A.src_frame;
   const uint32_t BI = D + kDescHeader + ((nm + 1) & ~1), TP = BI + 4 * nb;  // all even
@@ -209,15 +212,24 @@ __device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap
   float* g = A.dst + (long long)blockIdx.z * A.dst_frame;
   const unsigned n = (unsigned)A.n;
   const int ue = (U_r + lane) + A.gamma * (U_c + warp);
-  const unsigned ub = (unsigned)ue + A.bias;
+  unsigned ub = (unsigned)ue + A.bias;  // reduce E(u) mod n once per thread ...
+  for (int k = 0; k < A.nsub; ++k) ub = min(ub, ub - n);
 #pragma unroll
   for (int c = 0; c < MAXM; ++c) {
     if (grp * MAXM + c < nm && acc[c] != 0.f) {
-      unsigned P = ub + c_tab[D + kDescHeader + grp * MAXM + c];  // < (nsub + 1) * n
-      for (int k = 0; k < A.nsub; ++k) P = min(P, P - n);  // unsigned: subtracts n iff P >= n
+      unsigned P = ub + c_tab[D + kDescHeader + grp * MAXM + c];  // ... then once per mode: < 2n
+      P = min(P, P - n);
       atomicAdd(g + P, acc[c]);
     }
   }
+}
+
+template <int G, int MAXM, bool TMA>
+__device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap* tm) {
+  if (G == 2 && threadIdx.x >= kFwdThreads)
+    forward_group<G, MAXM, TMA, (G == 2 ? 1 : 0)>(A, tm);
+  else
+    forward_group<G, MAXM, TMA, 0>(A, tm);
 }
 
 // ------------------------------------------------------------------------------------------------
