@@ -380,6 +380,12 @@ ctis_status load_page(Page& pg, bool vec) {
     name = "ctis_back_b" + std::to_string(pg.max_modes) + (vec ? "_t" : "_s");
   }
   CTIS_CUDA(cudaLibraryGetKernel(&pg.kern, pg.lib, name.c_str()), "cudaLibraryGetKernel");
+  int dev = 0;
+  CTIS_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+  // deep window pipelines need more than the default 48 KB of dynamic shared memory
+  const int smem_max = pg.forward ? kFwdStages * kFwdWinFloats * 4 + 64 : kBackStages * kBackWinFloats * 4 + 64;
+  CTIS_CUDA(cudaKernelSetAttributeForDevice(pg.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max, dev),
+            "cudaKernelSetAttributeForDevice");
   return CTIS_OK;
 }
 
@@ -713,7 +719,8 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
     if (e != cudaSuccess) return e;
   }
   const int threads = fwd ? P.fwd_g * kFwdThreads : kBackThreads;
-  const size_t smem = (size_t)kStages * slot * sizeof(float) + 8 * kStages;
+  const int stages = fwd ? kFwdStages : kBackStages;
+  const size_t smem = (size_t)stages * slot * sizeof(float) + 8 * stages;
   for (const Page& pg : pages) {
     dim3 grid(pg.max_tiles, pg.nchunks, frames);
     void* args[] = {&A, &tm};

@@ -152,17 +152,17 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
   const float* f = A.src + (long long)blockIdx.z * A.src_frame;
   const uint32_t BI = D + kDescHeader + ((nm + 1) & ~1), TP = BI + 4 * nb;  // all even
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
-  const unsigned bars = sbase + kStages * A.slot_floats * 4u;  // kStages mbarriers after the slots
+  const unsigned bars = sbase + kFwdStages * A.slot_floats * 4u;  // kFwdStages mbarriers after the slots
 
   if (TMA) {
     if (threadIdx.x == 0) {
-      for (int s = 0; s < kStages; ++s) mbar_init(bars + 8 * s, 1);
+      for (int s = 0; s < kFwdStages; ++s) mbar_init(bars + 8 * s, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
   }
   auto issue = [&](int b) {
-    const int slot = b % kStages;
+    const int slot = b % kFwdStages;
     if (TMA) {
       if (b < nb && threadIdx.x == 0) {
         const uint32_t bi = BI + 4 * b;
@@ -185,14 +185,14 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
   for (int c = 0; c < MAXM; ++c) acc[c] = 0.f;
 
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) issue(s);
+  for (int s = 0; s < kFwdStages - 1; ++s) issue(s);
   for (int b = 0; b < nb; ++b) {
-    issue(b + kStages - 1);
-    const int slot = b % kStages;
+    issue(b + kFwdStages - 1);
+    const int slot = b % kFwdStages;
     if (TMA) {
-      mbar_wait(bars + 8 * slot, (unsigned)(b / kStages) & 1u);
+      mbar_wait(bars + 8 * slot, (unsigned)(b / kFwdStages) & 1u);
     } else {
-      cp_wait<kStages - 1>();
+      cp_wait<kFwdStages - 1>();
       __syncthreads();
     }
     // byte address of this thread's u in the window; tap entries hold byte offsets (absent: w = 0)
@@ -249,11 +249,11 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
   const float* r = A.src + (long long)blockIdx.z * A.src_frame;
   const uint32_t MI = D + kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * NB;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
-  const unsigned bars = sbase + kStages * A.slot_floats * 4u;
+  const unsigned bars = sbase + kBackStages * A.slot_floats * 4u;
 
   if (TMA) {
     if (threadIdx.x == 0) {
-      for (int s = 0; s < kStages; ++s) mbar_init(bars + 8 * s, 1);
+      for (int s = 0; s < kBackStages; ++s) mbar_init(bars + 8 * s, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -270,7 +270,7 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
     if (C0 >= A.xi) C0 -= A.xi;
   };
   auto issue = [&](int c) {
-    const int slot = c % kStages;
+    const int slot = c % kBackStages;
     if (c < nm) {
       int R0, C0;
       origin_rc(c, R0, C0);
@@ -299,14 +299,14 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
   for (int b = 0; b < NB; ++b) acc0[b] = acc1[b] = 0.f;
 
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) issue(s);
+  for (int s = 0; s < kBackStages - 1; ++s) issue(s);
   for (int c = 0; c < nm; ++c) {
-    issue(c + kStages - 1);
-    const int slot = c % kStages;
+    issue(c + kBackStages - 1);
+    const int slot = c % kBackStages;
     if (TMA) {
-      mbar_wait(bars + 8 * slot, (unsigned)(c / kStages) & 1u);
+      mbar_wait(bars + 8 * slot, (unsigned)(c / kBackStages) & 1u);
     } else {
-      cp_wait<kStages - 1>();
+      cp_wait<kBackStages - 1>();
       __syncthreads();
     }
     const int WR = tabi(MI + 4 * c + 2);
