@@ -383,7 +383,7 @@ ctis_status load_page(Page& pg, bool vec) {
   int dev = 0;
   CTIS_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
   // deep window pipelines need more than the default 48 KB of dynamic shared memory
-  const int smem_max = pg.forward ? kFwdStages * kFwdWinFloats * 4 + 64 : kBackStages * kBackWinFloats * 4 + 64;
+  const int smem_max = pg.forward ? kFwdStages * (kFwdWinFloats * 4 + 16) : kBackStages * (kBackWinFloats * 4 + 16);
   CTIS_CUDA(cudaKernelSetAttributeForDevice(pg.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max, dev),
             "cudaKernelSetAttributeForDevice");
   return CTIS_OK;
@@ -720,7 +720,7 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
   }
   const int threads = fwd ? P.fwd_g * kFwdThreads : kBackThreads;
   const int stages = fwd ? kFwdStages : kBackStages;
-  const size_t smem = (size_t)stages * slot * sizeof(float) + 8 * stages;
+  const size_t smem = (size_t)stages * slot * sizeof(float) + 16 * stages;  // + full/empty mbarriers
   for (const Page& pg : pages) {
     dim3 grid(pg.max_tiles, pg.nchunks, frames);
     void* args[] = {&A, &tm};

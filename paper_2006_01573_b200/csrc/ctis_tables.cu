@@ -141,6 +141,8 @@ __device__ __forceinline__ void load_r_window(float* buf, const float* r, const 
 template <int G, int MAXM, bool TMA, int GRP>
 __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMap* tm) {
   extern __shared__ __align__(128) float smem[];
+  constexpr int S = kFwdStages;
+  constexpr int NWARPS = G * kFwdThreads / 32;
   const uint32_t D = c_tab[1 + blockIdx.y];
   const int lam0 = tabi(D + 0), nb = tabi(D + 1), nm = tabi(D + 2);
   const int u_r0 = tabi(D + 3), u_c0 = tabi(D + 4), tiles_r = tabi(D + 5), tiles_c = tabi(D + 6);
@@ -152,51 +154,14 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
   const float* f = A.src + (long long)blockIdx.z * A.src_frame;
   const uint32_t BI = D + kDescHeader + ((nm + 1) & ~1), TP = BI + 4 * nb;  // all even
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
-  const unsigned bars = sbase + kFwdStages * A.slot_floats * 4u;  // kFwdStages mbarriers after the slots
-
-  if (TMA) {
-    if (threadIdx.x == 0) {
-      for (int s = 0; s < kFwdStages; ++s) mbar_init(bars + 8 * s, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-  }
-  auto issue = [&](int b) {
-    const int slot = b % kFwdStages;
-    if (TMA) {
-      if (b < nb && threadIdx.x == 0) {
-        const uint32_t bi = BI + 4 * b;
-        mbar_expect_tx(bars + 8 * slot, A.box_bytes);
-        tma_4d(sbase + 4u * slot * A.slot_floats, tm, U_r + tabi(bi + 0), U_c + tabi(bi + 1), lam0 + b,
-               (int)blockIdx.z, bars + 8 * slot);
-      }
-    } else {
-      if (b < nb) {
-        const uint32_t bi = BI + 4 * b;
-        load_f_window<G * kFwdThreads / 32>(smem + slot * A.slot_floats, f + (long long)(lam0 + b) * A.ell, A,
-                                        U_r + tabi(bi + 0), U_c + tabi(bi + 1), tabi(bi + 2), tabi(bi + 3));
-      }
-      cp_commit();  // one (possibly empty) group per band keeps the group arithmetic uniform
-    }
-  };
+  const unsigned full = sbase + S * A.slot_floats * 4u;  // S "full" then S "empty" mbarriers
+  const unsigned empty = full + 8 * S;
 
   float acc[MAXM];
 #pragma unroll
   for (int c = 0; c < MAXM; ++c) acc[c] = 0.f;
-
-#pragma unroll
-  for (int s = 0; s < kFwdStages - 1; ++s) issue(s);
-  for (int b = 0; b < nb; ++b) {
-    issue(b + kFwdStages - 1);
-    const int slot = b % kFwdStages;
-    if (TMA) {
-      mbar_wait(bars + 8 * slot, (unsigned)(b / kFwdStages) & 1u);
-    } else {
-      cp_wait<kFwdStages - 1>();
-      __syncthreads();
-    }
-    // byte address of this thread's u in the window; tap entries hold byte offsets (absent: w = 0)
-    const unsigned base = sbase + 4u * (slot * A.slot_floats + lane + tabi(BI + 4 * b + 2) * warp);
+  // one band: acc[mode] += w * window[u - shift(mode)]; entries hold byte offsets (absent: w = 0)
+  auto compute = [&](unsigned base, int b) {
     // pointer arithmetic (not an unsigned index) lets ptxas fold 8*c into LDCU.64 c[0x3][UR+imm]
     const uint2* ent = tab2(TP) + (b * G + grp) * MAXM;
 #pragma unroll
@@ -204,7 +169,59 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
       const uint2 e = ent[c];
       acc[c] = fmaf(__uint_as_float(e.y), lds(base + e.x), acc[c]);
     }
-    __syncthreads();  // every thread is done with this slot before it is refilled
+  };
+
+  if (TMA) {
+    // Full/empty mbarrier ring: thread 0 produces TMA boxes, every warp consumes and releases;
+    // warps only wait for data, never for each other.
+    auto issue = [&](int b) {
+      const int slot = b % S;
+      const uint32_t bi = BI + 4 * b;
+      mbar_expect_tx(full + 8 * slot, A.box_bytes);
+      tma_4d(sbase + 4u * slot * A.slot_floats, tm, U_r + tabi(bi + 0), U_c + tabi(bi + 1), lam0 + b,
+             (int)blockIdx.z, full + 8 * slot);
+    };
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < S; ++s) {
+        mbar_init(full + 8 * s, 1);
+        mbar_init(empty + 8 * s, NWARPS);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int b = 0; b < S && b < nb; ++b) issue(b);
+    }
+    __syncthreads();
+    const unsigned tbase = sbase + 4u * (lane + A.box_r * warp);
+    for (int b = 0; b < nb; ++b) {
+      const int slot = b % S;
+      mbar_wait(full + 8 * slot, (unsigned)(b / S) & 1u);
+      compute(tbase + 4u * slot * A.slot_floats, b);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + 8 * slot);
+      // refill the slot of band b-1 (one band of slack for slower warps) with band b-1+S
+      if (threadIdx.x == 0 && b >= 1 && b - 1 + S < nb) {
+        const int ps = (b - 1) % S;
+        mbar_wait(empty + 8 * ps, (unsigned)((b - 1) / S) & 1u);
+        issue(b - 1 + S);
+      }
+    }
+  } else {
+    auto issue = [&](int b) {
+      if (b < nb) {
+        const uint32_t bi = BI + 4 * b;
+        load_f_window<NWARPS>(smem + (b % S) * A.slot_floats, f + (long long)(lam0 + b) * A.ell, A,
+                              U_r + tabi(bi + 0), U_c + tabi(bi + 1), tabi(bi + 2), tabi(bi + 3));
+      }
+      cp_commit();  // one (possibly empty) group per band keeps the group arithmetic uniform
+    };
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) issue(s);
+    for (int b = 0; b < nb; ++b) {
+      issue(b + S - 1);
+      cp_wait<S - 1>();
+      __syncthreads();
+      compute(sbase + 4u * ((b % S) * A.slot_floats + lane + tabi(BI + 4 * b + 2) * warp), b);
+      __syncthreads();  // every thread is done with this slot before it is refilled
+    }
   }
   // flush: g_hat[(E(u) + o_ref) mod n] += acc.  E(u) = u_r + gamma*u_c can be negative (u reaches
   // kModeSpanMax outside the field stop); the host-chosen bias (a multiple of n) makes it >= 0, and
@@ -239,6 +256,8 @@ __device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap
 template <int NB, bool TMA>
 __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* tm) {
   extern __shared__ __align__(128) float smem[];
+  constexpr int S = kBackStages;
+  constexpr int NWARPS = kBackThreads / 32;
   const uint32_t D = c_tab[1 + blockIdx.y];
   const int lam0 = tabi(D + 0), nb = tabi(D + 1), nm = tabi(D + 2);
   const int tiles_r = tabi(D + 3), tiles_c = tabi(D + 4);
@@ -249,15 +268,9 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
   const float* r = A.src + (long long)blockIdx.z * A.src_frame;
   const uint32_t MI = D + kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * NB;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
-  const unsigned bars = sbase + kBackStages * A.slot_floats * 4u;
+  const unsigned full = sbase + S * A.slot_floats * 4u;
+  const unsigned empty = full + 8 * S;
 
-  if (TMA) {
-    if (threadIdx.x == 0) {
-      for (int s = 0; s < kBackStages; ++s) mbar_init(bars + 8 * s, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-  }
   // Window origin on the FPA: B = (tile1d + Bm) mod n as (R0, C0), from the host-split
   // Bm = Bm_r + gamma*Bm_c with one carry and one wrap (no division).
   auto origin_rc = [&](int c, int& R0, int& C0) {
@@ -269,49 +282,11 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
     }
     if (C0 >= A.xi) C0 -= A.xi;
   };
-  auto issue = [&](int c) {
-    const int slot = c % kBackStages;
-    if (c < nm) {
-      int R0, C0;
-      origin_rc(c, R0, C0);
-      if (TMA && R0 + A.box_r <= A.gamma && C0 + A.box_c <= A.xi) {
-        if (threadIdx.x == 0) {
-          mbar_expect_tx(bars + 8 * slot, A.box_bytes);
-          tma_3d(sbase + 4u * slot * A.slot_floats, tm, R0, C0, (int)blockIdx.z, bars + 8 * slot);
-        }
-      } else {  // element loads with exact modular indices (wrapped windows, unaligned geometries)
-        const unsigned B = (unsigned)R0 + (unsigned)A.gamma * (unsigned)C0;
-        const int WR = TMA ? A.box_r : tabi(MI + 4 * c + 2), WC = TMA ? A.box_c : tabi(MI + 4 * c + 3);
-        load_r_window<kBackThreads / 32>(smem + slot * A.slot_floats, r, A, B, WR, WC);
-        if (TMA) {  // complete the slot's phase by hand
-          cp_commit();
-          cp_wait<0>();
-          __syncthreads();
-          if (threadIdx.x == 0) mbar_arrive(bars + 8 * slot);
-        }
-      }
-    }
-    if (!TMA) cp_commit();
-  };
-
   float acc0[NB], acc1[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) acc0[b] = acc1[b] = 0.f;
-
-#pragma unroll
-  for (int s = 0; s < kBackStages - 1; ++s) issue(s);
-  for (int c = 0; c < nm; ++c) {
-    issue(c + kBackStages - 1);
-    const int slot = c % kBackStages;
-    if (TMA) {
-      mbar_wait(bars + 8 * slot, (unsigned)(c / kBackStages) & 1u);
-    } else {
-      cp_wait<kBackStages - 1>();
-      __syncthreads();
-    }
-    const int WR = tabi(MI + 4 * c + 2);
-    const unsigned b0a = sbase + 4u * (slot * A.slot_floats + lane + WR * warp);
-    const unsigned b1a = b0a + 4u * WR * (kBackThreads / 32);
+  // one mode: z[band] += w * window[q + shift(mode, band)] for 2 voxels (columns warp, warp+16)
+  auto compute = [&](unsigned b0a, unsigned b1a, int c) {
     const uint2* ent = tab2(TP) + c * NB;
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
@@ -320,10 +295,74 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
       acc0[b] = fmaf(w, lds(b0a + e.x), acc0[b]);
       acc1[b] = fmaf(w, lds(b1a + e.x), acc1[b]);
     }
+  };
+
+  // TMA is usable when every window of this tile is a plain FPA box (no carry / wrap of Eq. 7)
+  bool boxes = TMA;
+  if (TMA) {
+    for (int c = 0; c < nm && boxes; ++c) {
+      int R0, C0;
+      origin_rc(c, R0, C0);
+      boxes = (R0 + A.box_r <= A.gamma) && (C0 + A.box_c <= A.xi);
+    }
+  }
+  if (TMA && boxes) {
+    auto issue = [&](int c) {
+      const int slot = c % S;
+      int R0, C0;
+      origin_rc(c, R0, C0);
+      mbar_expect_tx(full + 8 * slot, A.box_bytes);
+      tma_3d(sbase + 4u * slot * A.slot_floats, tm, R0, C0, (int)blockIdx.z, full + 8 * slot);
+    };
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < S; ++s) {
+        mbar_init(full + 8 * s, 1);
+        mbar_init(empty + 8 * s, NWARPS);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int c = 0; c < S && c < nm; ++c) issue(c);
+    }
     __syncthreads();
+    const unsigned t0 = sbase + 4u * (lane + A.box_r * warp), t1 = t0 + 4u * A.box_r * NWARPS;
+    for (int c = 0; c < nm; ++c) {
+      const int slot = c % S;
+      mbar_wait(full + 8 * slot, (unsigned)(c / S) & 1u);
+      compute(t0 + 4u * slot * A.slot_floats, t1 + 4u * slot * A.slot_floats, c);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + 8 * slot);
+      if (threadIdx.x == 0 && c >= 1 && c - 1 + S < nm) {
+        const int ps = (c - 1) % S;
+        mbar_wait(empty + 8 * ps, (unsigned)((c - 1) / S) & 1u);
+        issue(c - 1 + S);
+      }
+    }
+  } else {
+    // element loads with exact modular indices (wrapped windows, unaligned geometries)
+    const int fixed_r = TMA ? A.box_r : 0, fixed_c = TMA ? A.box_c : 0;
+    auto issue = [&](int c) {
+      if (c < nm) {
+        int R0, C0;
+        origin_rc(c, R0, C0);
+        const unsigned B = (unsigned)R0 + (unsigned)A.gamma * (unsigned)C0;
+        load_r_window<NWARPS>(smem + (c % S) * A.slot_floats, r, A, B, TMA ? fixed_r : tabi(MI + 4 * c + 2),
+                              TMA ? fixed_c : tabi(MI + 4 * c + 3));
+      }
+      cp_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) issue(s);
+    for (int c = 0; c < nm; ++c) {
+      issue(c + S - 1);
+      cp_wait<S - 1>();
+      __syncthreads();
+      const int WR = TMA ? fixed_r : tabi(MI + 4 * c + 2);
+      const unsigned b0a = sbase + 4u * ((c % S) * A.slot_floats + lane + WR * warp);
+      compute(b0a, b0a + 4u * WR * NWARPS, c);
+      __syncthreads();
+    }
   }
   float* f = A.dst + (long long)blockIdx.z * A.dst_frame;
-  const int qr = q_r0 + lane, qc0 = q_c0 + warp, qc1 = qc0 + kBackThreads / 32;
+  const int qr = q_r0 + lane, qc0 = q_c0 + warp, qc1 = qc0 + NWARPS;
   if (qr >= A.a) return;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
