@@ -82,6 +82,16 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ unsigned atom_add_shared(unsigned addr, unsigned v) {
+  unsigned old;
+  asm volatile("atom.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_shared_u32(unsigned addr, unsigned v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 __device__ __forceinline__ void tma_3d(unsigned dst, const CUtensorMap* tm, int c0, int c1, int c2, unsigned bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
@@ -154,7 +164,7 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
   const float* f = A.src + (long long)blockIdx.z * A.src_frame;
   const uint32_t BI = D + kDescHeader + ((nm + 1) & ~1), TP = BI + 4 * nb;  // all even
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
-  const unsigned full = sbase + S * A.slot_floats * 4u;  // S "full" then S "empty" mbarriers
+  const unsigned full = sbase + S * A.slot_floats * 4u;  // S "full" mbarriers, then S release counters
   const unsigned empty = full + 8 * S;
 
   float acc[MAXM];
@@ -184,7 +194,7 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
     if (threadIdx.x == 0) {
       for (int s = 0; s < S; ++s) {
         mbar_init(full + 8 * s, 1);
-        mbar_init(empty + 8 * s, NWARPS);
+        st_shared_u32(empty + 4 * s, 0u);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       for (int b = 0; b < S && b < nb; ++b) issue(b);
@@ -196,12 +206,13 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
       mbar_wait(full + 8 * slot, (unsigned)(b / S) & 1u);
       compute(tbase + 4u * slot * A.slot_floats, b);
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty + 8 * slot);
-      // refill the slot of band b-1 (one band of slack for slower warps) with band b-1+S
-      if (threadIdx.x == 0 && b >= 1 && b - 1 + S < nb) {
-        const int ps = (b - 1) % S;
-        mbar_wait(empty + 8 * ps, (unsigned)((b - 1) / S) & 1u);
-        issue(b - 1 + S);
+      // the last warp to release the slot refills it with band b + S (no thread ever spins here)
+      if (lane == 0 && atom_add_shared(empty + 4 * slot, 1u) == NWARPS - 1) {
+        st_shared_u32(empty + 4 * slot, 0u);
+        if (b + S < nb) {
+          fence_proxy_async();
+          issue(b + S);
+        }
       }
     }
   } else {
@@ -317,7 +328,7 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
     if (threadIdx.x == 0) {
       for (int s = 0; s < S; ++s) {
         mbar_init(full + 8 * s, 1);
-        mbar_init(empty + 8 * s, NWARPS);
+        st_shared_u32(empty + 4 * s, 0u);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       for (int c = 0; c < S && c < nm; ++c) issue(c);
@@ -329,11 +340,12 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
       mbar_wait(full + 8 * slot, (unsigned)(c / S) & 1u);
       compute(t0 + 4u * slot * A.slot_floats, t1 + 4u * slot * A.slot_floats, c);
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty + 8 * slot);
-      if (threadIdx.x == 0 && c >= 1 && c - 1 + S < nm) {
-        const int ps = (c - 1) % S;
-        mbar_wait(empty + 8 * ps, (unsigned)((c - 1) / S) & 1u);
-        issue(c - 1 + S);
+      if (lane == 0 && atom_add_shared(empty + 4 * slot, 1u) == NWARPS - 1) {
+        st_shared_u32(empty + 4 * slot, 0u);
+        if (c + S < nm) {
+          fence_proxy_async();
+          issue(c + S);
+        }
       }
     }
   } else {
