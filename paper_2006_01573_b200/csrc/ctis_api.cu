@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -243,7 +244,7 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
   if (all.empty()) return true;  // no taps: nothing to emit
   const int tiles_r = (P.a + all.rmax - all.rmin + kFwdTR - 1) / kFwdTR;
   const int tiles_c = (P.alpha + all.cmax - all.cmin + kFwdTC - 1) / kFwdTC;
-  const int nm2 = (nm + 1) & ~1;  // keeps the tap entries at even word offsets (one LDCU.64 each)
+  const int nm2 = (nm + 3) & ~3;  // keeps the tap-pair entries 16-byte aligned
   out.assign(kDescHeader + nm2 + 4 * nb + 2 * nb * maxm, 0u);
   out[0] = (uint32_t)b0;
   out[1] = (uint32_t)nb;
@@ -278,8 +279,10 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
     for (const ModeTap& t : ms[c]->taps) {
       const int dr = t.dr - ms[c]->ref_dr, dc = t.dc - ms[c]->ref_dc;
       const int off = (sp[t.b].rmax + lead[t.b] - dr) + WRs[t.b] * (sp[t.b].cmax - dc);
-      out[TP + 2 * (t.b * maxm + c)] = (uint32_t)(4 * off);
-      out[TP + 2 * (t.b * maxm + c) + 1] = fbits(t.w);
+      // pair entry (off_{2k}, off_{2k+1}, w_{2k}, w_{2k+1}) of modes 2k, 2k+1 in band b
+      const int wi = TP + 4 * (t.b * (maxm / 2) + c / 2) + (c & 1);
+      out[wi] = (uint32_t)(4 * off);
+      out[wi + 2] = fbits(t.w);
     }
   tiles = tiles_r * tiles_c;
   return true;
@@ -289,7 +292,7 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
 bool back_desc(const ctis_plan_s& P, int b0, int nb, int NB, const std::vector<Mode>& ms,
                const std::vector<float>& invh, int box_r, int box_c, std::vector<uint32_t>& out, int& tiles) {
   const int nm = (int)ms.size();
-  out.assign(kDescHeader + 4 * nm + 2 * nm * NB + ((nb + 1) & ~1), 0u);  // even length
+  out.assign(kDescHeader + 4 * nm + 2 * nm * NB + ((nb + 3) & ~3), 0u);  // length % 4 == 0
   const int tiles_r = (P.a + kBackTR - 1) / kBackTR, tiles_c = (P.alpha + kBackTC - 1) / kBackTC;
   out[0] = (uint32_t)b0;
   out[1] = (uint32_t)nb;
@@ -317,8 +320,10 @@ bool back_desc(const ctis_plan_s& P, int b0, int nb, int NB, const std::vector<M
     out[MI + 4 * c + 3] = (uint32_t)WC;
     for (const ModeTap& t : md.taps) {
       const int dr = t.dr - md.ref_dr, dc = t.dc - md.ref_dc;
-      out[TP + 2 * (c * NB + t.b)] = (uint32_t)(4 * ((dr - sp.rmin + lead) + WR * (dc - sp.cmin)));
-      out[TP + 2 * (c * NB + t.b) + 1] = fbits(t.w);
+      // pair entry (off_{2k}, off_{2k+1}, w_{2k}, w_{2k+1}) of bands 2k, 2k+1 in mode c
+      const int wi = TP + 4 * (c * (NB / 2) + t.b / 2) + (t.b & 1);
+      out[wi] = (uint32_t)(4 * ((dr - sp.rmin + lead) + WR * (dc - sp.cmin)));
+      out[wi + 2] = fbits(t.w);
     }
   }
   for (int b = 0; b < nb; ++b) out[IH + b] = fbits(invh[b0 + b]);
@@ -425,8 +430,8 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
   // TMA needs 16-byte global strides: a % 4 == 0 for f, gamma % 4 == 0 for r.
   P.tma_f = (P.a % 4 == 0);
   P.tma_b = (P.gamma % 4 == 0);
-  // ---- forward: chunks of <= kFwdBands bands, modes split into passes of <= 96; one MAXM (nm rounded
-  //      up to 8) and one TMA box for the whole plan so that every forward page runs the same kernel
+  // ---- forward: chunks of <= kFwdBands bands, modes split into passes of <= 96; one kernel template
+  //      (G groups x MAXM modes, MAXM even: modes are paired for FFMA2) and one TMA box per plan
   {
     std::vector<std::vector<Mode>> chunk_modes;
     std::vector<std::pair<int, int>> chunks = balanced_chunks(P.w, kFwdBands);
@@ -440,10 +445,10 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     // the 1024-thread CTA within 64 registers); otherwise one group with up to 96 modes per pass.
     if (nm_max <= 64) {
       P.fwd_g = 2;
-      P.fwd_m = std::max(4, ((nm_max + 1) / 2 + 3) / 4 * 4);
+      P.fwd_m = std::max(2, ((nm_max + 1) / 2 + 1) / 2 * 2);
     } else {
       P.fwd_g = 1;
-      P.fwd_m = std::min(96, (nm_max + 7) / 8 * 8);
+      P.fwd_m = std::max(40, std::min(96, (nm_max + 7) / 8 * 8));
     }
     const int maxm = P.fwd_g * P.fwd_m;  // modes per pass
     std::vector<std::vector<const Mode*>> passes;
@@ -695,6 +700,14 @@ cudaError_t make_tensor_map(CUtensorMap* tm, bool forward, const ctis_plan_s& P,
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+int debug_flags() {
+  static int v = [] {
+    const char* e = std::getenv("CTIS_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const float* src, float* dst,
                          long long src_frame, long long dst_frame, int frames, int mode, cudaStream_t s,
                          int64_t* count) {
@@ -711,7 +724,7 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
   const int cap = fwd ? kFwdWinFloats : kBackWinFloats;
   const int slot = tma ? (box_r * box_c + 31) / 32 * 32 : cap;
   TabArgs A{src, dst, src_frame, dst_frame, P.a, P.alpha, P.gamma, P.xi, P.n, P.ell, mode, bias, nsub,
-            slot, box_r, box_c, (unsigned)(4 * box_r * box_c)};
+            slot, box_r, box_c, (unsigned)(4 * box_r * box_c), debug_flags()};
   alignas(64) CUtensorMap tm;
   std::memset(&tm, 0, sizeof(tm));
   if (tma) {

@@ -14,20 +14,22 @@ namespace ctis {
 // datapath (LDCU -> FFMA R, R, UR, R): tap metadata costs no L1/SMEM bandwidth.
 constexpr int kPageWords = 16384;  // 64 KB of uint32
 
-// Page layout (uint32 words; every descriptor starts and its tap entries sit at even offsets):
+// Page layout (uint32 words; descriptors and tap entries start at multiples of 4 words):
 //   [0]       number of chunks in the page
 //   [1 + k]   word offset of chunk k's descriptor
 //
 // Forward chunk descriptor (Eq. 12 evaluated per "mode"):
 //   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] u_r0   [D+4] u_c0   [D+5] tiles_r   [D+6] tiles_c  [D+7] G*MAXM
-//   [D+8 ..]            o_ref[c]                     (nm words rounded up to even, in [0, n))
-//   [BI = D+8+nm2 ..]   per band b: row0_rel, col0_rel, WR, WC   (window rows/cols relative to the tile)
-//   [TP = BI+4*nb ..]   per (b, g, c), c < MAXM: byte offset, w-bits (index TP + 2*((b*G + g)*MAXM + c));
-//                       mode = g*MAXM + c; w = 0 -> no tap; G, MAXM = the kernel template
+//   [D+8 ..]            o_ref[c]                     (nm words rounded up to a multiple of 4, in [0, n))
+//   [BI = D+8+nm4 ..]   per band b: row0_rel, col0_rel, WR, WC   (window rows/cols relative to the tile)
+//   [TP = BI+4*nb ..]   per band b and mode pair (2k, 2k+1) of the pass (G*MAXM modes): one 16-byte
+//                       entry (off_2k, off_2k+1, w_2k, w_2k+1) at TP + 4*(b*G*MAXM/2 + k); group g
+//                       owns pairs [g*MAXM/2, (g+1)*MAXM/2); w = 0 -> no tap
 // Back chunk descriptor (Eqs. 14-15):
 //   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] tiles_r   [D+4] tiles_c   [D+5] NB   [D+6..7] 0
 //   [MI = D+8 ..]       per mode c: Bm_r, Bm_c, WR, WC  (window origin term Bm = Bm_r + gamma*Bm_c in [0, n))
-//   [TP = MI+4*nm ..]   per (c, b), b < NB: byte offset, w-bits  (index TP + 2*(c*NB + b))
+//   [TP = MI+4*nm ..]   per mode c and band pair (2k, 2k+1): 16-byte entry (off_2k, off_2k+1,
+//                       w_2k, w_2k+1) at TP + 4*(c*NB/2 + k)
 //   [IH = TP+2*nm*NB ..] inv_h[b]
 enum : int { kDescHeader = 8 };
 
@@ -65,6 +67,7 @@ struct TabArgs {
   int slot_floats;     // floats per pipeline slot (multiple of 32)
   int box_r, box_c;    // TMA box (window) rows x columns; the window pitch is box_r
   unsigned box_bytes;  // 4 * box_r * box_c
+  int dbg;             // profiling switches (CTIS_DEBUG env): 1 = no TMA (compute on stale windows), 2 = no flush
 };
 
 }  // namespace ctis

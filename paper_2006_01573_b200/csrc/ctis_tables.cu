@@ -35,8 +35,9 @@ using namespace ctis;
 
 // 16-byte aligned so that tap entries (uint2 at even word offsets) load as one LDCU.64
 __constant__ __align__(16) uint32_t c_tab[kPageWords];
-__device__ __forceinline__ const uint2* tab2(uint32_t even_word) {
-  return reinterpret_cast<const uint2*>(c_tab) + (even_word >> 1);
+// Tap entries are 16-byte pairs (off0, off1, w0, w1) at word offsets that are multiples of 4.
+__device__ __forceinline__ const uint4* tab4(uint32_t word4) {
+  return reinterpret_cast<const uint4*>(c_tab) + (word4 >> 2);
 }
 
 namespace {
@@ -162,22 +163,25 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
   constexpr int grp = GRP;
   const int U_r = u_r0 + (tile % tiles_r) * kFwdTR, U_c = u_c0 + (tile / tiles_r) * kFwdTC;
   const float* f = A.src + (long long)blockIdx.z * A.src_frame;
-  const uint32_t BI = D + kDescHeader + ((nm + 1) & ~1), TP = BI + 4 * nb;  // all even
+  const uint32_t BI = D + kDescHeader + ((nm + 3) & ~3), TP = BI + 4 * nb;  // TP % 4 == 0
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
   const unsigned full = sbase + S * A.slot_floats * 4u;  // S "full" mbarriers, then S release counters
   const unsigned empty = full + 8 * S;
+  constexpr int MP = MAXM / 2;  // mode pairs: one FFMA2 (fp32x2) per pair
 
-  float acc[MAXM];
+  float2 acc[MP];
 #pragma unroll
-  for (int c = 0; c < MAXM; ++c) acc[c] = 0.f;
-  // one band: acc[mode] += w * window[u - shift(mode)]; entries hold byte offsets (absent: w = 0)
+  for (int k = 0; k < MP; ++k) acc[k] = make_float2(0.f, 0.f);
+  // one band: acc[mode] += w * window[u - shift(mode)]; entries hold byte offsets (absent: w = 0).
+  // Pointer arithmetic lets ptxas fold the entry offset into LDCU.64 c[0x3][UR+imm]; the weight
+  // pair feeds FFMA2 R, R.F32x2, UR.F32x2, R.F32x2 straight from the uniform registers.
   auto compute = [&](unsigned base, int b) {
-    // pointer arithmetic (not an unsigned index) lets ptxas fold 8*c into LDCU.64 c[0x3][UR+imm]
-    const uint2* ent = tab2(TP) + (b * G + grp) * MAXM;
+    const uint4* ent = tab4(TP) + (b * G + grp) * MP;
 #pragma unroll
-    for (int c = 0; c < MAXM; ++c) {
-      const uint2 e = ent[c];
-      acc[c] = fmaf(__uint_as_float(e.y), lds(base + e.x), acc[c]);
+    for (int k = 0; k < MP; ++k) {
+      const uint4 e = ent[k];
+      const float2 x = make_float2(lds(base + e.x), lds(base + e.y));
+      acc[k] = __ffma2_rn(make_float2(__uint_as_float(e.z), __uint_as_float(e.w)), x, acc[k]);
     }
   };
 
@@ -197,19 +201,20 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
         st_shared_u32(empty + 4 * s, 0u);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int b = 0; b < S && b < nb; ++b) issue(b);
+      if (!(A.dbg & 1))
+        for (int b = 0; b < S && b < nb; ++b) issue(b);
     }
     __syncthreads();
     const unsigned tbase = sbase + 4u * (lane + A.box_r * warp);
     for (int b = 0; b < nb; ++b) {
       const int slot = b % S;
-      mbar_wait(full + 8 * slot, (unsigned)(b / S) & 1u);
+      if (!(A.dbg & 1)) mbar_wait(full + 8 * slot, (unsigned)(b / S) & 1u);
       compute(tbase + 4u * slot * A.slot_floats, b);
       __syncwarp();
       // the last warp to release the slot refills it with band b + S (no thread ever spins here)
       if (lane == 0 && atom_add_shared(empty + 4 * slot, 1u) == NWARPS - 1) {
         st_shared_u32(empty + 4 * slot, 0u);
-        if (b + S < nb) {
+        if (b + S < nb && !(A.dbg & 1)) {
           fence_proxy_async();
           issue(b + S);
         }
@@ -240,14 +245,22 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
   float* g = A.dst + (long long)blockIdx.z * A.dst_frame;
   const unsigned n = (unsigned)A.n;
   const int ue = (U_r + lane) + A.gamma * (U_c + warp);
+  if (A.dbg & 2) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < MP; ++k) t += acc[k].x + acc[k].y;
+    if (t == -1.f) g[0] = t;
+    return;
+  }
   unsigned ub = (unsigned)ue + A.bias;  // reduce E(u) mod n once per thread ...
   for (int k = 0; k < A.nsub; ++k) ub = min(ub, ub - n);
 #pragma unroll
   for (int c = 0; c < MAXM; ++c) {
-    if (grp * MAXM + c < nm && acc[c] != 0.f) {
+    const float v = (c & 1) ? acc[c >> 1].y : acc[c >> 1].x;
+    if (grp * MAXM + c < nm && v != 0.f) {
       unsigned P = ub + c_tab[D + kDescHeader + grp * MAXM + c];  // ... then once per mode: < 2n
       P = min(P, P - n);
-      atomicAdd(g + P, acc[c]);
+      atomicAdd(g + P, v);
     }
   }
 }
@@ -293,18 +306,19 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
     }
     if (C0 >= A.xi) C0 -= A.xi;
   };
-  float acc0[NB], acc1[NB];
+  constexpr int BP = NB / 2;  // band pairs: one FFMA2 (fp32x2) per pair and voxel
+  float2 acc0[BP], acc1[BP];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) acc0[b] = acc1[b] = 0.f;
+  for (int k = 0; k < BP; ++k) acc0[k] = acc1[k] = make_float2(0.f, 0.f);
   // one mode: z[band] += w * window[q + shift(mode, band)] for 2 voxels (columns warp, warp+16)
   auto compute = [&](unsigned b0a, unsigned b1a, int c) {
-    const uint2* ent = tab2(TP) + c * NB;
+    const uint4* ent = tab4(TP) + c * BP;
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const uint2 e = ent[b];
-      const float w = __uint_as_float(e.y);
-      acc0[b] = fmaf(w, lds(b0a + e.x), acc0[b]);
-      acc1[b] = fmaf(w, lds(b1a + e.x), acc1[b]);
+    for (int k = 0; k < BP; ++k) {
+      const uint4 e = ent[k];
+      const float2 w = make_float2(__uint_as_float(e.z), __uint_as_float(e.w));
+      acc0[k] = __ffma2_rn(w, make_float2(lds(b0a + e.x), lds(b0a + e.y)), acc0[k]);
+      acc1[k] = __ffma2_rn(w, make_float2(lds(b1a + e.x), lds(b1a + e.y)), acc1[k]);
     }
   };
 
@@ -331,18 +345,19 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
         st_shared_u32(empty + 4 * s, 0u);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int c = 0; c < S && c < nm; ++c) issue(c);
+      if (!(A.dbg & 1))
+        for (int c = 0; c < S && c < nm; ++c) issue(c);
     }
     __syncthreads();
     const unsigned t0 = sbase + 4u * (lane + A.box_r * warp), t1 = t0 + 4u * A.box_r * NWARPS;
     for (int c = 0; c < nm; ++c) {
       const int slot = c % S;
-      mbar_wait(full + 8 * slot, (unsigned)(c / S) & 1u);
+      if (!(A.dbg & 1)) mbar_wait(full + 8 * slot, (unsigned)(c / S) & 1u);
       compute(t0 + 4u * slot * A.slot_floats, t1 + 4u * slot * A.slot_floats, c);
       __syncwarp();
       if (lane == 0 && atom_add_shared(empty + 4 * slot, 1u) == NWARPS - 1) {
         st_shared_u32(empty + 4 * slot, 0u);
-        if (c + S < nm) {
+        if (c + S < nm && !(A.dbg & 1)) {
           fence_proxy_async();
           issue(c + S);
         }
@@ -381,13 +396,15 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
     if (b < nb) {
       const long long lb = (long long)(lam0 + b) * A.ell + qr;
       const float ih = tabf(IH + b);
+      const float z0 = (b & 1) ? acc0[b >> 1].y : acc0[b >> 1].x;
+      const float z1 = (b & 1) ? acc1[b >> 1].y : acc1[b >> 1].x;
       if (qc0 < A.alpha) {
         float* p = f + lb + (long long)A.a * qc0;
-        *p = A.mode ? (*p) * acc0[b] * ih : acc0[b];
+        *p = A.mode ? (*p) * z0 * ih : z0;
       }
       if (qc1 < A.alpha) {
         float* p = f + lb + (long long)A.a * qc1;
-        *p = A.mode ? (*p) * acc1[b] * ih : acc1[b];
+        *p = A.mode ? (*p) * z1 * ih : z1;
       }
     }
   }
@@ -404,18 +421,22 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
       ctis_fwd_g##G##_m##M##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                  \
     forward_body<G, M, false>(A, &tm);                                                                     \
   }
+CTIS_FWD(2, 2)
 CTIS_FWD(2, 4)
+CTIS_FWD(2, 6)
 CTIS_FWD(2, 8)
+CTIS_FWD(2, 10)
 CTIS_FWD(2, 12)
+CTIS_FWD(2, 14)
 CTIS_FWD(2, 16)
+CTIS_FWD(2, 18)
 CTIS_FWD(2, 20)
+CTIS_FWD(2, 22)
 CTIS_FWD(2, 24)
+CTIS_FWD(2, 26)
 CTIS_FWD(2, 28)
+CTIS_FWD(2, 30)
 CTIS_FWD(2, 32)
-CTIS_FWD(1, 8)
-CTIS_FWD(1, 16)
-CTIS_FWD(1, 24)
-CTIS_FWD(1, 32)
 CTIS_FWD(1, 40)
 CTIS_FWD(1, 48)
 CTIS_FWD(1, 56)
