@@ -443,7 +443,8 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     }
     // <= 64 modes: two 16-warp groups split the modes (MAXM per group, multiple of 4, <= 32, keeps
     // the 1024-thread CTA within 64 registers); otherwise one group with up to 96 modes per pass.
-    if (nm_max <= 64) {
+    const char* force_g = std::getenv("CTIS_FWD_GROUPS");
+    if (nm_max <= 64 && !(force_g && std::atoi(force_g) == 1)) {
       P.fwd_g = 2;
       P.fwd_m = std::max(2, ((nm_max + 1) / 2 + 1) / 2 * 2);
     } else {

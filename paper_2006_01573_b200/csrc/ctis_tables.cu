@@ -195,29 +195,35 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
       tma_4d(sbase + 4u * slot * A.slot_floats, tm, U_r + tabi(bi + 0), U_c + tabi(bi + 1), lam0 + b,
              (int)blockIdx.z, full + 8 * slot);
     };
+    // Batched refills: S = 2K slots; every K bands one CTA barrier (all warps are done with the
+    // previous K bands), then thread 0 issues the next K boxes.  The tap loop itself has no
+    // spinning producer and no atomics, so its control flow stays warp-uniform.
+    constexpr int K = S / 2;
     if (threadIdx.x == 0) {
-      for (int s = 0; s < S; ++s) {
-        mbar_init(full + 8 * s, 1);
-        st_shared_u32(empty + 4 * s, 0u);
-      }
+      for (int s = 0; s < S; ++s) mbar_init(full + 8 * s, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       if (!(A.dbg & 1))
         for (int b = 0; b < S && b < nb; ++b) issue(b);
     }
     __syncthreads();
     const unsigned tbase = sbase + 4u * (lane + A.box_r * warp);
+    const unsigned slot_bytes = 4u * A.slot_floats;
+    int slot = 0;
+    unsigned phase = 0;
     for (int b = 0; b < nb; ++b) {
-      const int slot = b % S;
-      if (!(A.dbg & 1)) mbar_wait(full + 8 * slot, (unsigned)(b / S) & 1u);
-      compute(tbase + 4u * slot * A.slot_floats, b);
-      __syncwarp();
-      // the last warp to release the slot refills it with band b + S (no thread ever spins here)
-      if (lane == 0 && atom_add_shared(empty + 4 * slot, 1u) == NWARPS - 1) {
-        st_shared_u32(empty + 4 * slot, 0u);
-        if (b + S < nb && !(A.dbg & 1)) {
-          fence_proxy_async();
-          issue(b + S);
+      if (b >= K && b % K == 0) {
+        __syncthreads();
+        if (threadIdx.x == 0 && !(A.dbg & 1)) {
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            if (b + K + k < nb) issue(b + K + k);
         }
+      }
+      if (!(A.dbg & 1)) mbar_wait(full + 8 * slot, phase);
+      compute(tbase + slot * slot_bytes, b);
+      if (++slot == S) {
+        slot = 0;
+        phase ^= 1u;
       }
     }
   } else {
@@ -339,28 +345,32 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
       mbar_expect_tx(full + 8 * slot, A.box_bytes);
       tma_3d(sbase + 4u * slot * A.slot_floats, tm, R0, C0, (int)blockIdx.z, full + 8 * slot);
     };
+    constexpr int K = S / 2;  // batched refills, as in the forward kernel
     if (threadIdx.x == 0) {
-      for (int s = 0; s < S; ++s) {
-        mbar_init(full + 8 * s, 1);
-        st_shared_u32(empty + 4 * s, 0u);
-      }
+      for (int s = 0; s < S; ++s) mbar_init(full + 8 * s, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       if (!(A.dbg & 1))
         for (int c = 0; c < S && c < nm; ++c) issue(c);
     }
     __syncthreads();
     const unsigned t0 = sbase + 4u * (lane + A.box_r * warp), t1 = t0 + 4u * A.box_r * NWARPS;
+    const unsigned slot_bytes = 4u * A.slot_floats;
+    int slot = 0;
+    unsigned phase = 0;
     for (int c = 0; c < nm; ++c) {
-      const int slot = c % S;
-      if (!(A.dbg & 1)) mbar_wait(full + 8 * slot, (unsigned)(c / S) & 1u);
-      compute(t0 + 4u * slot * A.slot_floats, t1 + 4u * slot * A.slot_floats, c);
-      __syncwarp();
-      if (lane == 0 && atom_add_shared(empty + 4 * slot, 1u) == NWARPS - 1) {
-        st_shared_u32(empty + 4 * slot, 0u);
-        if (c + S < nm && !(A.dbg & 1)) {
-          fence_proxy_async();
-          issue(c + S);
+      if (c >= K && c % K == 0) {
+        __syncthreads();
+        if (threadIdx.x == 0 && !(A.dbg & 1)) {
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            if (c + K + k < nm) issue(c + K + k);
         }
+      }
+      if (!(A.dbg & 1)) mbar_wait(full + 8 * slot, phase);
+      compute(t0 + slot * slot_bytes, t1 + slot * slot_bytes, c);
+      if (++slot == S) {
+        slot = 0;
+        phase ^= 1u;
       }
     }
   } else {

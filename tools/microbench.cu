@@ -121,7 +121,7 @@ __constant__ uint2 c_taps[4096];
 __device__ __forceinline__ float lds_u(unsigned a) { float v; asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a)); return v; }
 
 // JIT-style tap loop: LDS [R + imm] and FFMA with an immediate weight.
-__global__ void __launch_bounds__(512, 2) taps_imm_kernel(int iters, float* out) {
+__global__ void __launch_bounds__(512, 4) taps_imm_kernel(int iters, float* out) {
   extern __shared__ float s[];
   for (int i = threadIdx.x; i < 8192; i += blockDim.x) s[i] = (float)i;
   __syncthreads();
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(512, 2) taps_imm_kernel(int iters, float* out)
 }
 
 // Table-style tap loop: (offset, weight) from __constant__ via the uniform datapath.
-__global__ void __launch_bounds__(512, 2) taps_ldcu_kernel(int iters, float* out) {
+__global__ void __launch_bounds__(512, 4) taps_ldcu_kernel(int iters, float* out) {
   extern __shared__ float s[];
   for (int i = threadIdx.x; i < 8192; i += blockDim.x) s[i] = (float)i;
   __syncthreads();
@@ -271,6 +271,15 @@ int main() {
     printf(", \"taps_imm_fma_per_clk_per_sm\": %.2f\n", fmas / (ms * 1e-3) / sms / (mhz * 1e6));
     ms = time_ms([&] { taps_ldcu_kernel<<<blocks, threads, 40 * 1024>>>(it, out); });
     printf(", \"taps_ldcu_fma_per_clk_per_sm\": %.2f\n", fmas / (ms * 1e-3) / sms / (mhz * 1e6));
+    // occupancy sweep: 1..4 CTAs of 512 threads per SM (smaller shared allocation)
+    for (int occ = 1; occ <= 4; ++occ) {
+      const int b2 = sms * occ;
+      const double f2 = (double)b2 * threads * it * 64;
+      ms = time_ms([&] { taps_imm_kernel<<<b2, threads, 33 * 1024>>>(it, out); });
+      printf(", \"taps_imm_occ%d\": %.2f\n", occ, f2 / (ms * 1e-3) / sms / (mhz * 1e6));
+      ms = time_ms([&] { taps_ldcu_kernel<<<b2, threads, 33 * 1024>>>(it, out); });
+      printf(", \"taps_ldcu_occ%d\": %.2f\n", occ, f2 / (ms * 1e-3) / sms / (mhz * 1e6));
+    }
   }
   // L2 streaming read (64 MB buffer, resident)
   {
