@@ -49,8 +49,8 @@ constexpr int kBackBandsMax = 16;
 // Mode shifts are bounded by kModeSpan (|dr|, |dc| <= 12 from the mode reference), so a window
 // never exceeds (32 + 24 + 3 -> 60) x (16 + 24) floats (forward) or 60 x (32 + 24) (back).
 constexpr int kModeSpanMax = 12;
-constexpr int kFwdStages = 6;           // window pipeline depth (TMA boxes / cp.async groups in flight),
-constexpr int kBackStages = 6;          // refilled K = stages/2 at a time
+constexpr int kFwdStages = 8;           // window pipeline depth (TMA boxes / cp.async groups in flight),
+constexpr int kBackStages = 8;          // refilled K = stages/2 at a time
 constexpr int kFwdWinFloats = 2560;     // 10 KB per stage (>= 60 x 40)
 constexpr int kBackWinFloats = 3584;    // 14 KB per stage (>= 60 x 56)
 

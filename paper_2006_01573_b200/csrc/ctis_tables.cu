@@ -197,8 +197,10 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
     };
     // Batched refills: S = 2K slots; every K bands one CTA barrier (all warps are done with the
     // previous K bands), then thread 0 issues the next K boxes.  The tap loop itself has no
-    // spinning producer and no atomics, so its control flow stays warp-uniform.
+    // spinning producer and no atomics, so its control flow stays warp-uniform; it handles two
+    // bands per trip (K is even) to amortise the per-trip bookkeeping over 2*MAXM taps.
     constexpr int K = S / 2;
+    static_assert(K % 2 == 0, "two bands per trip");
     if (threadIdx.x == 0) {
       for (int s = 0; s < S; ++s) mbar_init(full + 8 * s, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -210,7 +212,8 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
     const unsigned slot_bytes = 4u * A.slot_floats;
     int slot = 0;
     unsigned phase = 0;
-    for (int b = 0; b < nb; ++b) {
+    int b = 0;
+    for (; b + 1 < nb; b += 2) {
       if (b >= K && b % K == 0) {
         __syncthreads();
         if (threadIdx.x == 0 && !(A.dbg & 1)) {
@@ -219,12 +222,25 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
             if (b + K + k < nb) issue(b + K + k);
         }
       }
-      if (!(A.dbg & 1)) mbar_wait(full + 8 * slot, phase);
+      if (!(A.dbg & 1)) {
+        mbar_wait(full + 8 * slot, phase);
+        mbar_wait(full + 8 * (slot + 1), phase);
+      }
       compute(tbase + slot * slot_bytes, b);
-      if (++slot == S) {
+      compute(tbase + (slot + 1) * slot_bytes, b + 1);
+      slot += 2;
+      if (slot == S) {
         slot = 0;
         phase ^= 1u;
       }
+    }
+    if (b < nb) {  // odd band count: last band alone (its box was issued by the last refill)
+      if (b >= K && b % K == 0) {
+        __syncthreads();
+        if (threadIdx.x == 0 && !(A.dbg & 1) && b + K < nb) issue(b + K);
+      }
+      if (!(A.dbg & 1)) mbar_wait(full + 8 * slot, phase);
+      compute(tbase + slot * slot_bytes, b);
     }
   } else {
     auto issue = [&](int b) {
@@ -345,7 +361,8 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
       mbar_expect_tx(full + 8 * slot, A.box_bytes);
       tma_3d(sbase + 4u * slot * A.slot_floats, tm, R0, C0, (int)blockIdx.z, full + 8 * slot);
     };
-    constexpr int K = S / 2;  // batched refills, as in the forward kernel
+    constexpr int K = S / 2;  // batched refills and two modes per trip, as in the forward kernel
+    static_assert(K % 2 == 0, "two modes per trip");
     if (threadIdx.x == 0) {
       for (int s = 0; s < S; ++s) mbar_init(full + 8 * s, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -357,7 +374,8 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
     const unsigned slot_bytes = 4u * A.slot_floats;
     int slot = 0;
     unsigned phase = 0;
-    for (int c = 0; c < nm; ++c) {
+    int c = 0;
+    for (; c + 1 < nm; c += 2) {
       if (c >= K && c % K == 0) {
         __syncthreads();
         if (threadIdx.x == 0 && !(A.dbg & 1)) {
@@ -366,12 +384,25 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
             if (c + K + k < nm) issue(c + K + k);
         }
       }
-      if (!(A.dbg & 1)) mbar_wait(full + 8 * slot, phase);
+      if (!(A.dbg & 1)) {
+        mbar_wait(full + 8 * slot, phase);
+        mbar_wait(full + 8 * (slot + 1), phase);
+      }
       compute(t0 + slot * slot_bytes, t1 + slot * slot_bytes, c);
-      if (++slot == S) {
+      compute(t0 + (slot + 1) * slot_bytes, t1 + (slot + 1) * slot_bytes, c + 1);
+      slot += 2;
+      if (slot == S) {
         slot = 0;
         phase ^= 1u;
       }
+    }
+    if (c < nm) {
+      if (c >= K && c % K == 0) {
+        __syncthreads();
+        if (threadIdx.x == 0 && !(A.dbg & 1) && c + K < nm) issue(c + K);
+      }
+      if (!(A.dbg & 1)) mbar_wait(full + 8 * slot, phase);
+      compute(t0 + slot * slot_bytes, t1 + slot * slot_bytes, c);
     }
   } else {
     // element loads with exact modular indices (wrapped windows, unaligned geometries)

@@ -1,0 +1,117 @@
+// tapbench.cu — which shared-memory tap-loop structure runs fastest on sm_100a?
+// Each variant: NACC accumulators, TAPS taps per "band" (one pass over all accumulators per band when
+// TAPS == NACC), tap metadata (byte offset, weight) from __constant__ via the uniform datapath, an
+// LDS per tap from a static window, FFMA (or FFMA2 on pairs).  Reports FMA/clk/SM.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+__constant__ __align__(16) unsigned c_t[16384];
+
+__device__ __forceinline__ float lds(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+
+template <int NACC, bool PAIR, int MINB>
+__global__ void __launch_bounds__(512, MINB) k(int bands, int tab_words, float* out) {
+  extern __shared__ float smem[];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) smem[i] = 1.0f + i * 1e-6f;
+  __syncthreads();
+  const unsigned base = (unsigned)__cvta_generic_to_shared(smem) + 4u * threadIdx.x;
+  float acc[NACC];
+#pragma unroll
+  for (int c = 0; c < NACC; ++c) acc[c] = 0.f;
+  for (int b = 0; b < bands; ++b) {
+    const unsigned wofs = (unsigned)((b * NACC * 2) % (tab_words - NACC * 2));
+    if (PAIR) {
+      const uint4* e4 = reinterpret_cast<const uint4*>(c_t) + (wofs >> 2);
+#pragma unroll
+      for (int c = 0; c < NACC / 2; ++c) {
+        const uint4 e = e4[c];
+        float2 a = make_float2(acc[2 * c], acc[2 * c + 1]);
+        a = __ffma2_rn(make_float2(__uint_as_float(e.z), __uint_as_float(e.w)), make_float2(lds(base + e.x), lds(base + e.y)), a);
+        acc[2 * c] = a.x;
+        acc[2 * c + 1] = a.y;
+      }
+    } else {
+      const uint2* e2 = reinterpret_cast<const uint2*>(c_t) + (wofs >> 1);
+#pragma unroll
+      for (int c = 0; c < NACC; ++c) {
+        const uint2 e = e2[c];
+        acc[c] = fmaf(__uint_as_float(e.y), lds(base + e.x), acc[c]);
+      }
+    }
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int c = 0; c < NACC; ++c) t += acc[c];
+  if (t == 1.2345f) out[0] = t;
+}
+
+template <int NACC, bool PAIR, int MINB>
+void run(const char* name, int sms, double mhz, float* out, int tab_words) {
+  const int bands = 4096;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int occ = 1; occ <= 2; ++occ) {
+    const int blocks = sms * occ;
+    k<NACC, PAIR, MINB><<<blocks, 512, 40 * 1024>>>(bands, tab_words, out);
+    cudaDeviceSynchronize();
+    float best = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+      cudaEventRecord(a);
+      k<NACC, PAIR, MINB><<<blocks, 512, 40 * 1024>>>(bands, tab_words, out);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      best = ms < best ? ms : best;
+    }
+    const double fmas = (double)blocks * 512 * bands * NACC;
+    printf("%-22s tab=%6dB occ=%d  %.2f FMA/clk/SM\n", name, tab_words * 4, occ, fmas / (best * 1e-3) / sms / (mhz * 1e6));
+  }
+}
+
+int main() {
+  cudaDeviceProp p;
+  cudaGetDeviceProperties(&p, 0);
+  const int sms = p.multiProcessorCount;
+  const double mhz = 1965.0;
+  float* out;
+  cudaMalloc(&out, 64);
+  std::vector<unsigned> h(16384);
+  for (int i = 0; i < 16384; ++i) {
+    float w = 0.5f;
+    unsigned wb;
+    memcpy(&wb, &w, 4);
+    h[i] = (i % 2 == 0) ? 4u * ((i * 37u) % 1536u) : wb;
+  }
+  // PAIR layout (off0, off1, w0, w1): fix words
+  std::vector<unsigned> hp(16384);
+  for (int i = 0; i < 16384; i += 4) {
+    float w = 0.5f;
+    unsigned wb;
+    memcpy(&wb, &w, 4);
+    hp[i] = 4u * ((i * 37u) % 1536u);
+    hp[i + 1] = 4u * ((i * 53u + 7) % 1536u);
+    hp[i + 2] = wb;
+    hp[i + 3] = wb;
+  }
+  for (int tw : {512, 4096, 16384}) {
+    cudaMemcpyToSymbol(c_t, h.data(), 65536);
+    for (int i = 0; i < 2; ++i) cudaFuncSetAttribute(k<16, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
+    run<16, false, 1>("acc16 ffma", sms, mhz, out, tw);
+    run<28, false, 1>("acc28 ffma", sms, mhz, out, tw);
+    run<56, false, 1>("acc56 ffma", sms, mhz, out, tw);
+    cudaMemcpyToSymbol(c_t, hp.data(), 65536);
+    run<16, true, 1>("acc16 ffma2", sms, mhz, out, tw);
+    run<28, true, 1>("acc28 ffma2", sms, mhz, out, tw);
+    run<56, true, 1>("acc56 ffma2", sms, mhz, out, tw);
+  }
+  return 0;
+}
