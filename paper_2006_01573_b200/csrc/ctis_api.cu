@@ -69,6 +69,7 @@ struct GraphKey {
 // One 64 KB __constant__ page of tap tables and the library instance that owns it.
 struct Page {
   bool forward = true;
+  bool pair = false;
   int nchunks = 0;
   int max_tiles = 0;
   int max_modes = 0;
@@ -90,6 +91,7 @@ struct ctis_plan_s {
   int back_nb = kBackBandsMax;
   int fbox_r = 0, fbox_c = 0, bbox_r = 0, bbox_c = 0;
   int fwd_g = 1, fwd_m = 8;
+  bool pair = false;  // FFMA2 on tap pairs (16-byte entries) or plain FFMA (8-byte entries)
   std::vector<Page> fwd, back;
   float* d_hband = nullptr;
   int* d_flag = nullptr;
@@ -279,10 +281,11 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
     for (const ModeTap& t : ms[c]->taps) {
       const int dr = t.dr - ms[c]->ref_dr, dc = t.dc - ms[c]->ref_dc;
       const int off = (sp[t.b].rmax + lead[t.b] - dr) + WRs[t.b] * (sp[t.b].cmax - dc);
-      // pair entry (off_{2k}, off_{2k+1}, w_{2k}, w_{2k+1}) of modes 2k, 2k+1 in band b
-      const int wi = TP + 4 * (t.b * (maxm / 2) + c / 2) + (c & 1);
+      // pair layout: (off_{2k}, off_{2k+1}, w_{2k}, w_{2k+1}) of modes 2k, 2k+1 in band b (FFMA2);
+      // plain layout: (off_c, w_c) per mode
+      const int wi = P.pair ? TP + 4 * (t.b * (maxm / 2) + c / 2) + (c & 1) : TP + 2 * (t.b * maxm + c);
       out[wi] = (uint32_t)(4 * off);
-      out[wi + 2] = fbits(t.w);
+      out[wi + (P.pair ? 2 : 1)] = fbits(t.w);
     }
   tiles = tiles_r * tiles_c;
   return true;
@@ -320,10 +323,10 @@ bool back_desc(const ctis_plan_s& P, int b0, int nb, int NB, const std::vector<M
     out[MI + 4 * c + 3] = (uint32_t)WC;
     for (const ModeTap& t : md.taps) {
       const int dr = t.dr - md.ref_dr, dc = t.dc - md.ref_dc;
-      // pair entry (off_{2k}, off_{2k+1}, w_{2k}, w_{2k+1}) of bands 2k, 2k+1 in mode c
-      const int wi = TP + 4 * (c * (NB / 2) + t.b / 2) + (t.b & 1);
+      // pair layout (off_{2k}, off_{2k+1}, w_{2k}, w_{2k+1}) of bands 2k, 2k+1 (FFMA2); plain (off, w)
+      const int wi = P.pair ? TP + 4 * (c * (NB / 2) + t.b / 2) + (t.b & 1) : TP + 2 * (c * NB + t.b);
       out[wi] = (uint32_t)(4 * ((dr - sp.rmin + lead) + WR * (dc - sp.cmin)));
-      out[wi + 2] = fbits(t.w);
+      out[wi + (P.pair ? 2 : 1)] = fbits(t.w);
     }
   }
   for (int b = 0; b < nb; ++b) out[IH + b] = fbits(invh[b0 + b]);
@@ -428,6 +431,7 @@ int choose_back_nb(const ctis_plan_s& P) {
 
 ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& bands, const std::vector<float>& invh) {
   // TMA needs 16-byte global strides: a % 4 == 0 for f, gamma % 4 == 0 for r.
+  P.pair = true;  // FFMA2 on tap pairs (plain FFMA measured no faster on B200)
   P.tma_f = (P.a % 4 == 0);
   P.tma_b = (P.gamma % 4 == 0);
   // ---- forward: chunks of <= kFwdBands bands, modes split into passes of <= 96; one kernel template
@@ -443,15 +447,20 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     }
     // <= 64 modes: two 16-warp groups split the modes (MAXM per group, multiple of 4, <= 32, keeps
     // the 1024-thread CTA within 64 registers); otherwise one group with up to 96 modes per pass.
+    // <= 64 modes: each pass holds half of them (MAXM even, <= 32) and runs as two independent
+    // 512-thread CTAs per SM, one per pass (G = 1, default: a CTA's prologue, first-window latency
+    // and flush overlap the other CTA's tap loop; measured 78 vs 95 us at C4), or as one 1024-thread
+    // CTA with two mode groups sharing each window (G = 2; CTIS_FWD_GROUPS=2).
     const char* force_g = std::getenv("CTIS_FWD_GROUPS");
-    if (nm_max <= 64 && !(force_g && std::atoi(force_g) == 1)) {
-      P.fwd_g = 2;
+    if (nm_max <= 64) {
+      P.fwd_g = (force_g && std::atoi(force_g) == 2) ? 2 : 1;
       P.fwd_m = std::max(2, ((nm_max + 1) / 2 + 1) / 2 * 2);
     } else {
       P.fwd_g = 1;
       P.fwd_m = std::max(40, std::min(96, (nm_max + 7) / 8 * 8));
     }
-    const int maxm = P.fwd_g * P.fwd_m;  // modes per pass
+    // modes per pass (G = 1 with a small MAXM: two passes of MAXM modes)
+    const int maxm = (P.fwd_g == 1 && P.fwd_m <= 32) ? P.fwd_m : P.fwd_g * P.fwd_m;
     std::vector<std::vector<const Mode*>> passes;
     std::vector<int> pass_chunk;
     for (size_t k = 0; k < chunk_modes.size(); ++k)
@@ -540,10 +549,12 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     pack_pages(P.back, false, descs, tiles, nbs);
   }
   for (Page& pg : P.fwd) {
+    pg.pair = P.pair;
     ctis_status st = load_page(pg, P.tma_f);
     if (st) return st;
   }
   for (Page& pg : P.back) {
+    pg.pair = P.pair;
     ctis_status st = load_page(pg, P.tma_b);
     if (st) return st;
   }

@@ -149,7 +149,7 @@ __device__ __forceinline__ void load_r_window(float* buf, const float* r, const 
 // G groups of 16 warps share every window; group GRP owns modes [GRP*MAXM, (GRP+1)*MAXM) of the
 // pass.  GRP is a template parameter (dispatched on a warp-uniform branch) so that the tap-table
 // pointer stays uniform and the entries load through LDCU.64 rather than per-thread LDC.
-template <int G, int MAXM, bool TMA, int GRP>
+template <int G, int MAXM, bool TMA, int GRP, bool PAIR>
 __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMap* tm) {
   extern __shared__ __align__(128) float smem[];
   constexpr int S = kFwdStages;
@@ -176,12 +176,22 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
   // Pointer arithmetic lets ptxas fold the entry offset into LDCU.64 c[0x3][UR+imm]; the weight
   // pair feeds FFMA2 R, R.F32x2, UR.F32x2, R.F32x2 straight from the uniform registers.
   auto compute = [&](unsigned base, int b) {
-    const uint4* ent = tab4(TP) + (b * G + grp) * MP;
+    if (PAIR) {
+      const uint4* ent = tab4(TP) + (b * G + grp) * MP;
 #pragma unroll
-    for (int k = 0; k < MP; ++k) {
-      const uint4 e = ent[k];
-      const float2 x = make_float2(lds(base + e.x), lds(base + e.y));
-      acc[k] = __ffma2_rn(make_float2(__uint_as_float(e.z), __uint_as_float(e.w)), x, acc[k]);
+      for (int k = 0; k < MP; ++k) {
+        const uint4 e = ent[k];
+        const float2 x = make_float2(lds(base + e.x), lds(base + e.y));
+        acc[k] = __ffma2_rn(make_float2(__uint_as_float(e.z), __uint_as_float(e.w)), x, acc[k]);
+      }
+    } else {  // plain FFMA, 8-byte (offset, weight) entries
+      const uint2* ent = reinterpret_cast<const uint2*>(tab4(TP)) + (b * G + grp) * MAXM;
+#pragma unroll
+      for (int k = 0; k < MP; ++k) {
+        const uint2 e0 = ent[2 * k], e1 = ent[2 * k + 1];
+        acc[k].x = fmaf(__uint_as_float(e0.y), lds(base + e0.x), acc[k].x);
+        acc[k].y = fmaf(__uint_as_float(e1.y), lds(base + e1.x), acc[k].y);
+      }
     }
   };
 
@@ -287,19 +297,19 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
   }
 }
 
-template <int G, int MAXM, bool TMA>
+template <int G, int MAXM, bool TMA, bool PAIR>
 __device__ __forceinline__ void forward_body(const TabArgs& A, const CUtensorMap* tm) {
   if (G == 2 && threadIdx.x >= kFwdThreads)
-    forward_group<G, MAXM, TMA, (G == 2 ? 1 : 0)>(A, tm);
+    forward_group<G, MAXM, TMA, (G == 2 ? 1 : 0), PAIR>(A, tm);
   else
-    forward_group<G, MAXM, TMA, 0>(A, tm);
+    forward_group<G, MAXM, TMA, 0, PAIR>(A, tm);
 }
 
 // ------------------------------------------------------------------------------------------------
 // Back.  TMA: r viewed as a 3-D tensor {gamma, xi, frames}; a window whose 1-D origin B = (R0, C0)
 // on the FPA fits without carry/wrap (R0 + WRbox <= gamma, C0 + WCbox <= xi) is one box load; any
 // other window (cyclic wrap of Eq. 7) is loaded element by element with exact modular indices.
-template <int NB, bool TMA>
+template <int NB, bool TMA, bool PAIR>
 __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* tm) {
   extern __shared__ __align__(128) float smem[];
   constexpr int S = kBackStages;
@@ -334,13 +344,26 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
   for (int k = 0; k < BP; ++k) acc0[k] = acc1[k] = make_float2(0.f, 0.f);
   // one mode: z[band] += w * window[q + shift(mode, band)] for 2 voxels (columns warp, warp+16)
   auto compute = [&](unsigned b0a, unsigned b1a, int c) {
-    const uint4* ent = tab4(TP) + c * BP;
+    if (PAIR) {
+      const uint4* ent = tab4(TP) + c * BP;
 #pragma unroll
-    for (int k = 0; k < BP; ++k) {
-      const uint4 e = ent[k];
-      const float2 w = make_float2(__uint_as_float(e.z), __uint_as_float(e.w));
-      acc0[k] = __ffma2_rn(w, make_float2(lds(b0a + e.x), lds(b0a + e.y)), acc0[k]);
-      acc1[k] = __ffma2_rn(w, make_float2(lds(b1a + e.x), lds(b1a + e.y)), acc1[k]);
+      for (int k = 0; k < BP; ++k) {
+        const uint4 e = ent[k];
+        const float2 w = make_float2(__uint_as_float(e.z), __uint_as_float(e.w));
+        acc0[k] = __ffma2_rn(w, make_float2(lds(b0a + e.x), lds(b0a + e.y)), acc0[k]);
+        acc1[k] = __ffma2_rn(w, make_float2(lds(b1a + e.x), lds(b1a + e.y)), acc1[k]);
+      }
+    } else {  // plain FFMA, 8-byte (offset, weight) entries
+      const uint2* ent = reinterpret_cast<const uint2*>(tab4(TP)) + c * NB;
+#pragma unroll
+      for (int k = 0; k < BP; ++k) {
+        const uint2 e0 = ent[2 * k], e1 = ent[2 * k + 1];
+        const float w0 = __uint_as_float(e0.y), w1 = __uint_as_float(e1.y);
+        acc0[k].x = fmaf(w0, lds(b0a + e0.x), acc0[k].x);
+        acc1[k].x = fmaf(w0, lds(b1a + e0.x), acc1[k].x);
+        acc0[k].y = fmaf(w1, lds(b0a + e1.x), acc0[k].y);
+        acc1[k].y = fmaf(w1, lds(b1a + e1.x), acc1[k].y);
+      }
     }
   };
 
@@ -453,48 +476,64 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
 
 }  // namespace
 
-#define CTIS_FWD(G, M)                                                                                     \
-  extern "C" __global__ void __launch_bounds__(G * kFwdThreads, 1)                                         \
+#define CTIS_FWD(G, M, MINB)                                                                               \
+  extern "C" __global__ void __launch_bounds__(G * kFwdThreads, MINB)                                      \
       ctis_fwd_g##G##_m##M##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                  \
-    forward_body<G, M, true>(A, &tm);                                                                      \
+    forward_body<G, M, true, true>(A, &tm);                                                                \
   }                                                                                                        \
-  extern "C" __global__ void __launch_bounds__(G * kFwdThreads, 1)                                         \
+  extern "C" __global__ void __launch_bounds__(G * kFwdThreads, MINB)                                      \
       ctis_fwd_g##G##_m##M##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                  \
-    forward_body<G, M, false>(A, &tm);                                                                     \
+    forward_body<G, M, false, true>(A, &tm);                                                               \
   }
-CTIS_FWD(2, 2)
-CTIS_FWD(2, 4)
-CTIS_FWD(2, 6)
-CTIS_FWD(2, 8)
-CTIS_FWD(2, 10)
-CTIS_FWD(2, 12)
-CTIS_FWD(2, 14)
-CTIS_FWD(2, 16)
-CTIS_FWD(2, 18)
-CTIS_FWD(2, 20)
-CTIS_FWD(2, 22)
-CTIS_FWD(2, 24)
-CTIS_FWD(2, 26)
-CTIS_FWD(2, 28)
-CTIS_FWD(2, 30)
-CTIS_FWD(2, 32)
-CTIS_FWD(1, 40)
-CTIS_FWD(1, 48)
-CTIS_FWD(1, 56)
-CTIS_FWD(1, 64)
-CTIS_FWD(1, 72)
-CTIS_FWD(1, 80)
-CTIS_FWD(1, 88)
-CTIS_FWD(1, 96)
+CTIS_FWD(2, 2, 1)
+CTIS_FWD(2, 4, 1)
+CTIS_FWD(2, 6, 1)
+CTIS_FWD(2, 8, 1)
+CTIS_FWD(2, 10, 1)
+CTIS_FWD(2, 12, 1)
+CTIS_FWD(2, 14, 1)
+CTIS_FWD(2, 16, 1)
+CTIS_FWD(2, 18, 1)
+CTIS_FWD(2, 20, 1)
+CTIS_FWD(2, 22, 1)
+CTIS_FWD(2, 24, 1)
+CTIS_FWD(2, 26, 1)
+CTIS_FWD(2, 28, 1)
+CTIS_FWD(2, 30, 1)
+CTIS_FWD(2, 32, 1)
+CTIS_FWD(1, 2, 2)
+CTIS_FWD(1, 4, 2)
+CTIS_FWD(1, 6, 2)
+CTIS_FWD(1, 8, 2)
+CTIS_FWD(1, 10, 2)
+CTIS_FWD(1, 12, 2)
+CTIS_FWD(1, 14, 2)
+CTIS_FWD(1, 16, 2)
+CTIS_FWD(1, 18, 2)
+CTIS_FWD(1, 20, 2)
+CTIS_FWD(1, 22, 2)
+CTIS_FWD(1, 24, 2)
+CTIS_FWD(1, 26, 2)
+CTIS_FWD(1, 28, 2)
+CTIS_FWD(1, 30, 2)
+CTIS_FWD(1, 32, 2)
+CTIS_FWD(1, 40, 1)
+CTIS_FWD(1, 48, 1)
+CTIS_FWD(1, 56, 1)
+CTIS_FWD(1, 64, 1)
+CTIS_FWD(1, 72, 1)
+CTIS_FWD(1, 80, 1)
+CTIS_FWD(1, 88, 1)
+CTIS_FWD(1, 96, 1)
 
 #define CTIS_BACK(NB)                                                                                      \
   extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
       ctis_back_b##NB##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                       \
-    back_body<NB, true>(A, &tm);                                                                           \
+    back_body<NB, true, true>(A, &tm);                                                                     \
   }                                                                                                        \
   extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
       ctis_back_b##NB##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                       \
-    back_body<NB, false>(A, &tm);                                                                          \
+    back_body<NB, false, true>(A, &tm);                                                                    \
   }
 CTIS_BACK(4)
 CTIS_BACK(8)
