@@ -260,7 +260,10 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
   const int BI = kDescHeader + nm2, TP = BI + 4 * nb;
   std::vector<int> WRs(nb, 1), lead(nb, 0);
   for (int b = 0; b < nb; ++b) {
-    if (sp[b].empty()) {  // band without taps in this pass: any window, never read
+    if (sp[b].empty()) {  // band without taps in this pass: never read, but the TMA box origin
+      // must still be 16-byte aligned (row origin all.rmin + 32k - lead = multiple of 4)
+      out[BI + 4 * b + 0] = (uint32_t)(-(int)((((long long)all.rmin % 4) + 4) % 4));
+      out[BI + 4 * b + 1] = 0u;
       out[BI + 4 * b + 2] = (uint32_t)std::max(box_r, 1);
       out[BI + 4 * b + 3] = box_r ? (uint32_t)box_c : 0u;
       continue;

@@ -15,9 +15,9 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv \
      --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e \
      > gpurun_out/${TAG}_ncu_bench.txt 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:ctis_fwd -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:ctis_fwd -s 2 -c 1 \
      -o gpurun_out/${TAG}_prof_fwd -f python tools/prof_driver.py > gpurun_out/${TAG}_ncu_fwd.txt 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:ctis_back -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:ctis_back -s 2 -c 1 \
      -o gpurun_out/${TAG}_prof_back -f python tools/prof_driver.py > gpurun_out/${TAG}_ncu_back.txt 2>&1
 fi
 echo done
