@@ -73,12 +73,13 @@ struct Page {
   int nchunks = 0;
   int max_tiles = 0;
   int max_modes = 0;
+  int total_items = 0;  // tiles summed over the page's chunks (persistent kernels)
   std::vector<uint32_t> words;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
 };
 
-constexpr int kPageHeader = 64;  // word 0 = nchunks, words 1..63 = chunk descriptor offsets
+constexpr int kPageHeader = kPageHeaderWords;  // nchunks, descriptor offsets, item prefix sums
 
 }  // namespace
 
@@ -91,6 +92,7 @@ struct ctis_plan_s {
   int back_nb = kBackBandsMax;
   int fbox_r = 0, fbox_c = 0, bbox_r = 0, bbox_c = 0;
   int fwd_g = 1, fwd_m = 8;
+  int sms = 148;
   bool pair = false;  // FFMA2 on tap pairs (16-byte entries) or plain FFMA (8-byte entries)
   std::vector<Page> fwd, back;
   float* d_hband = nullptr;
@@ -350,12 +352,14 @@ void pack_pages(std::vector<Page>& pages, bool forward, const std::vector<std::v
       cur.forward = forward;
       cur.words.assign(kPageHeader, 0u);
     }
-    if (cur.nchunks == kPageHeader - 1 || cur.words.size() + descs[i].size() > (size_t)kPageWords) {
+    if (cur.nchunks == kItemBase - 1 || cur.words.size() + descs[i].size() > (size_t)kPageWords) {
       flush();
       cur.forward = forward;
       cur.words.assign(kPageHeader, 0u);
     }
     cur.words[1 + cur.nchunks] = (uint32_t)cur.words.size();
+    cur.words[kItemBase + cur.nchunks + 1] = cur.words[kItemBase + cur.nchunks] + (uint32_t)tiles[i];
+    cur.total_items += tiles[i];
     cur.words.insert(cur.words.end(), descs[i].begin(), descs[i].end());
     cur.nchunks++;
     cur.words[0] = (uint32_t)cur.nchunks;
@@ -454,9 +458,8 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     // 512-thread CTAs per SM, one per pass (G = 1, default: a CTA's prologue, first-window latency
     // and flush overlap the other CTA's tap loop; measured 78 vs 95 us at C4), or as one 1024-thread
     // CTA with two mode groups sharing each window (G = 2; CTIS_FWD_GROUPS=2).
-    const char* force_g = std::getenv("CTIS_FWD_GROUPS");
     if (nm_max <= 64) {
-      P.fwd_g = (force_g && std::atoi(force_g) == 2) ? 2 : 1;
+      P.fwd_g = 1;
       P.fwd_m = std::max(2, ((nm_max + 1) / 2 + 1) / 2 * 2);
     } else {
       P.fwd_g = 1;
@@ -524,6 +527,32 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     }
     P.bbox_r = box_r;
     P.bbox_c = box_c;
+    // The persistent TMA back kernel needs every window of every tile to be a plain FPA box (no
+    // carry / wrap of Eq. 7); otherwise the plan uses the exact element-loader kernels.
+    if (P.tma_b) {
+      const int tiles_r = (P.a + kBackTR - 1) / kBackTR, tiles_c = (P.alpha + kBackTC - 1) / kBackTC;
+      for (const auto& ms : cms) {
+        for (const Mode& md : ms) {
+          const Span sp = mode_span(md);
+          const long long B0 = (long long)md.ref_dr + (long long)P.gamma * md.ref_dc + sp.rmin +
+                               (long long)P.gamma * sp.cmin;
+          const int lead = (int)(((B0 % 4) + 4) % 4);
+          long long Bm = (B0 - lead) % P.n;
+          if (Bm < 0) Bm += P.n;
+          const int br = (int)(Bm % P.gamma), bc = (int)(Bm / P.gamma);
+          for (int tc = 0; tc < tiles_c && P.tma_b; ++tc)
+            for (int tr = 0; tr < tiles_r && P.tma_b; ++tr) {
+              int R0 = tr * kBackTR + br, C0 = tc * kBackTC + bc;
+              if (R0 >= P.gamma) {
+                R0 -= P.gamma;
+                C0 += 1;
+              }
+              if (C0 >= P.xi) C0 -= P.xi;
+              if (R0 + box_r > P.gamma || C0 + box_c > P.xi) P.tma_b = false;
+            }
+        }
+      }
+    }
     std::vector<std::vector<uint32_t>> descs;
     std::vector<int> tiles;
     for (size_t k = 0; k < todo.size(); ++k) {
@@ -608,6 +637,7 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
 
   DeviceGuard dg(device);
   auto* p = new ctis_plan_s();
+  p->sms = prop.multiProcessorCount;
   p->device = device;
   p->shard = shard;
   p->band_begin = b0;
@@ -739,7 +769,7 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
   const int cap = fwd ? kFwdWinFloats : kBackWinFloats;
   const int slot = tma ? (box_r * box_c + 31) / 32 * 32 : cap;
   TabArgs A{src, dst, src_frame, dst_frame, P.a, P.alpha, P.gamma, P.xi, P.n, P.ell, mode, bias, nsub,
-            slot, box_r, box_c, (unsigned)(4 * box_r * box_c), debug_flags()};
+            slot, box_r, box_c, (unsigned)(4 * box_r * box_c), debug_flags(), frames};
   alignas(64) CUtensorMap tm;
   std::memset(&tm, 0, sizeof(tm));
   if (tma) {
@@ -749,8 +779,13 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
   const int threads = fwd ? P.fwd_g * kFwdThreads : kBackThreads;
   const int stages = fwd ? kFwdStages : kBackStages;
   const size_t smem = (size_t)stages * slot * sizeof(float) + 16 * stages;  // + full/empty mbarriers
+  A.frames = frames;
   for (const Page& pg : pages) {
-    dim3 grid(pg.max_tiles, pg.nchunks, frames);
+    // TMA kernels are persistent (2 CTAs per SM walk the page's items); element-loader kernels are
+    // one CTA per (tile, chunk, frame)
+    const long long items = (long long)pg.total_items * frames;
+    dim3 grid = tma ? dim3((unsigned)std::min<long long>(items, 2LL * P.sms), 1, 1)
+                    : dim3(pg.max_tiles, pg.nchunks, frames);
     void* args[] = {&A, &tm};
     cudaError_t e = cudaLaunchKernel((const void*)pg.kern, grid, dim3(threads), args, smem, s);
     if (e != cudaSuccess) return e;

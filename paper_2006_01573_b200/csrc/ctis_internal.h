@@ -15,8 +15,9 @@ namespace ctis {
 constexpr int kPageWords = 16384;  // 64 KB of uint32
 
 // Page layout (uint32 words; descriptors and tap entries start at multiples of 4 words):
-//   [0]       number of chunks in the page
+//   [0]       number of chunks in the page (<= 63)
 //   [1 + k]   word offset of chunk k's descriptor
+//   [kItemBase + k]  work items (tiles) of chunks 0..k-1 (prefix sums); [kItemBase + nch] = total
 //
 // Forward chunk descriptor (Eq. 12 evaluated per "mode"):
 //   [D+0] lam0   [D+1] nb   [D+2] nm   [D+3] u_r0   [D+4] u_c0   [D+5] tiles_r   [D+6] tiles_c  [D+7] G*MAXM
@@ -31,7 +32,7 @@ constexpr int kPageWords = 16384;  // 64 KB of uint32
 //   [TP = MI+4*nm ..]   per mode c and band pair (2k, 2k+1): 16-byte entry (off_2k, off_2k+1,
 //                       w_2k, w_2k+1) at TP + 4*(c*NB/2 + k)
 //   [IH = TP+2*nm*NB ..] inv_h[b]
-enum : int { kDescHeader = 8 };
+enum : int { kDescHeader = 8, kItemBase = 64, kPageHeaderWords = 128 };
 
 // Forward kernel geometry: one u-space position per thread, 32 rows x 16 columns per CTA; a CTA
 // has G in {1, 2} groups of kFwdThreads threads that share each window and split the modes.
@@ -68,6 +69,7 @@ struct TabArgs {
   int box_r, box_c;    // TMA box (window) rows x columns; the window pitch is box_r
   unsigned box_bytes;  // 4 * box_r * box_c
   int dbg;             // profiling switches (CTIS_DEBUG env): 1 = no TMA (compute on stale windows), 2 = no flush
+  int frames;          // persistent kernels: frames in the launch (items = frames x page items)
 };
 
 }  // namespace ctis

@@ -52,6 +52,65 @@ __global__ void __launch_bounds__(512, MINB) k(int bands, int tab_words, float* 
   if (t == 1.2345f) out[0] = t;
 }
 
+// Mirror of the forward kernel's loop: MP pairs per band, 2 bands per trip, ring of 8 window slots of
+// SLOT floats, CTA barrier every 4 bands, tap table walked band by band (working set ~ 4 bands).
+template <int MP, int MINB>
+__global__ void __launch_bounds__(512, MINB) kf(int bands, float* out) {
+  extern __shared__ float smem[];
+  constexpr int SLOT = 2400;
+  for (int i = threadIdx.x; i < 8 * SLOT; i += blockDim.x) smem[i] = 1.0f + i * 1e-6f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned tbase = (unsigned)__cvta_generic_to_shared(smem) + 4u * (lane + 60 * warp);
+  float2 acc[MP];
+#pragma unroll
+  for (int k = 0; k < MP; ++k) acc[k] = make_float2(0.f, 0.f);
+  int slot = 0;
+  for (int b = 0; b + 1 < bands; b += 2) {
+    if (b >= 4 && b % 4 == 0) __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint4* e4 = reinterpret_cast<const uint4*>(c_t) + ((b + h) % 64) * MP;
+      const unsigned base = tbase + 4u * (slot + h) * SLOT;
+#pragma unroll
+      for (int k = 0; k < MP; ++k) {
+        const uint4 e = e4[k];
+        acc[k] = __ffma2_rn(make_float2(__uint_as_float(e.z), __uint_as_float(e.w)), make_float2(lds(base + e.x), lds(base + e.y)), acc[k]);
+      }
+    }
+    slot += 2;
+    if (slot == 8) slot = 0;
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int k = 0; k < MP; ++k) t += acc[k].x + acc[k].y;
+  if (t == 1.2345f) out[0] = t;
+}
+
+template <int MP, int MINB>
+void runf(const char* name, int sms, double mhz, float* out, int bands) {
+  cudaFuncSetAttribute(kf<MP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2400 * 4);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int blocks = sms * MINB;
+  kf<MP, MINB><<<blocks, 512, 8 * 2400 * 4>>>(bands, out);
+  cudaDeviceSynchronize();
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    cudaEventRecord(a);
+    kf<MP, MINB><<<blocks, 512, 8 * 2400 * 4>>>(bands, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    best = ms < best ? ms : best;
+  }
+  const double fmas = (double)blocks * 512 * (bands / 2 * 2) * 2 * MP;
+  printf("%-22s bands=%5d occ=%d  %.2f FMA/clk/SM  (%s)\n", name, bands, MINB, fmas / (best * 1e-3) / sms / (mhz * 1e6),
+         cudaGetErrorString(cudaGetLastError()));
+}
+
 template <int NACC, bool PAIR, int MINB>
 void run(const char* name, int sms, double mhz, float* out, int tab_words) {
   const int bands = 4096;
@@ -102,7 +161,25 @@ int main() {
     hp[i + 2] = wb;
     hp[i + 3] = wb;
   }
-  for (int tw : {512, 4096, 16384}) {
+  {
+    std::vector<unsigned> hp2(16384);
+    for (int i = 0; i < 16384; i += 4) {
+      float w = 0.5f;
+      unsigned wb;
+      memcpy(&wb, &w, 4);
+      hp2[i] = 4u * ((i * 37u) % 1400u);
+      hp2[i + 1] = 4u * ((i * 53u + 7) % 1400u);
+      hp2[i + 2] = wb;
+      hp2[i + 3] = wb;
+    }
+    cudaMemcpyToSymbol(c_t, hp2.data(), 65536);
+    runf<13, 2>("fwd-like mp13", sms, mhz, out, 16);
+    runf<13, 2>("fwd-like mp13", sms, mhz, out, 256);
+    runf<13, 2>("fwd-like mp13", sms, mhz, out, 4096);
+    runf<13, 1>("fwd-like mp13", sms, mhz, out, 4096);
+    runf<28, 1>("fwd-like mp28", sms, mhz, out, 4096);
+  }
+  for (int tw : {512}) {
     cudaMemcpyToSymbol(c_t, h.data(), 65536);
     for (int i = 0; i < 2; ++i) cudaFuncSetAttribute(k<16, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
     run<16, false, 1>("acc16 ffma", sms, mhz, out, tw);
