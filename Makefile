@@ -1,6 +1,5 @@
 # Builds the CUDA hot path (libctis.so, sm_100a) and the CPU oracle (liboracle.so).
 NVCC     ?= /usr/local/cuda/bin/nvcc
-BIN2C    ?= /usr/local/cuda/bin/bin2c
 PKG      := paper_2006_01573_b200
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden \
@@ -15,17 +14,20 @@ build/ctis_tables.cubin: $(PKG)/csrc/ctis_tables.cu $(HDRS)
 	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Iinclude -cubin -Xptxas -v $< -o $@ 2> build/ctis_tables.ptxas.log \
 	  || (cat build/ctis_tables.ptxas.log; false)
 
-build/ctis_tables_cubin.h: build/ctis_tables.cubin
-	$(BIN2C) --const --name ctis_tables_cubin $< > $@
+# embedded with .incbin (assembling a 10 MB array literal through nvcc takes minutes)
+build/ctis_tables_blob.o: build/ctis_tables.cubin
+	printf '.section .rodata\n.balign 16\n.globl ctis_tables_cubin\n.globl ctis_tables_cubin_end\n.hidden ctis_tables_cubin\n.hidden ctis_tables_cubin_end\nctis_tables_cubin:\n.incbin "%s"\nctis_tables_cubin_end:\n.byte 0\n.section .note.GNU-stack,"",@progbits\n' $(abspath $<) > build/ctis_tables_blob.S
+	gcc -c build/ctis_tables_blob.S -o $@
 
-build/ctis_api.o: $(PKG)/csrc/ctis_api.cu build/ctis_tables_cubin.h $(HDRS)
+build/ctis_api.o: $(PKG)/csrc/ctis_api.cu $(HDRS)
+	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 build/ctis_kernels.o: $(PKG)/csrc/ctis_kernels.cu $(HDRS)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> build/ctis_kernels.ptxas.log || (cat build/ctis_kernels.ptxas.log; false)
 
-$(PKG)/libctis.so: build/ctis_api.o build/ctis_kernels.o
+$(PKG)/libctis.so: build/ctis_api.o build/ctis_kernels.o build/ctis_tables_blob.o
 	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC -o $@.tmp $^ && mv $@.tmp $@
 
 oracle/liboracle.so: oracle/ctis_oracle.c

@@ -18,7 +18,8 @@
 #include "../../include/ctis.h"
 #include "ctis_internal.h"
 #include "ctis_kernels.h"
-#include "ctis_tables_cubin.h"  // generated: unsigned char ctis_tables_cubin[] (bin2c)
+// the projection-kernel cubin, embedded by build/ctis_tables_blob.S (.incbin)
+extern "C" const unsigned char ctis_tables_cubin[], ctis_tables_cubin_end[];
 
 using namespace ctis;
 
@@ -145,9 +146,9 @@ struct Mode {
 };
 
 constexpr int kModeTrack = 3;   // max band-to-band move of a mode (pixels, Chebyshev)
-constexpr int kModeSpan = kModeSpanMax;  // max |shift| of a tap from its mode reference (pixels)
 
-std::vector<Mode> cluster_modes(const std::vector<std::vector<TapXY>>& bands) {
+// span: max |shift| of a tap from its mode reference (pixels, Chebyshev)
+std::vector<Mode> cluster_modes(const std::vector<std::vector<TapXY>>& bands, int span = kModeSpanDefault) {
   const int nb = (int)bands.size();
   const int bref = (nb - 1) / 2;
   std::vector<Mode> modes;
@@ -176,7 +177,7 @@ std::vector<Mode> cluster_modes(const std::vector<std::vector<TapXY>>& bands) {
         const int ldr = up ? md.hi_dr : md.lo_dr, ldc = up ? md.hi_dc : md.lo_dc;
         const int d = std::max(std::abs(t.dr - ldr), std::abs(t.dc - ldc));
         const int s = std::max(std::abs(t.dr - md.ref_dr), std::abs(t.dc - md.ref_dc));
-        if (d <= kModeTrack && s <= kModeSpan && d < bestd) {
+        if (d <= kModeTrack && s <= span && d < bestd) {
           best = i;
           bestd = d;
         }
@@ -275,7 +276,9 @@ bool forward_desc(const ctis_plan_s& P, int b0, int nb, const std::vector<const 
     lead[b] = box_r ? (int)((((long long)all.rmin - sp[b].rmax) % 4 + 4) % 4) : 0;
     const int WR = box_r ? box_r : kFwdTR + sp[b].rmax - sp[b].rmin;
     const int WC = box_r ? box_c : kFwdTC + sp[b].cmax - sp[b].cmin;
-    if (WR * WC > kFwdWinFloats || (box_r && kFwdTR + sp[b].rmax - sp[b].rmin + lead[b] > box_r)) return false;
+    if (WR * WC > (box_r ? kTmaWinFloats : kFwdWinFloats) ||
+        (box_r && kFwdTR + sp[b].rmax - sp[b].rmin + lead[b] > box_r))
+      return false;
     WRs[b] = WR;
     out[BI + 4 * b + 0] = (uint32_t)(-sp[b].rmax - lead[b]);
     out[BI + 4 * b + 1] = (uint32_t)(-sp[b].cmax);
@@ -369,24 +372,59 @@ void pack_pages(std::vector<Page>& pages, bool forward, const std::vector<std::v
   flush();
 }
 
-const void* tables_image() {
-  // 8-byte aligned copy of the embedded cubin (bin2c emits a byte array).
-  static std::vector<uint64_t> img = [] {
-    std::vector<uint64_t> v((sizeof(ctis_tables_cubin) + 7) / 8, 0);
-    std::memcpy(v.data(), ctis_tables_cubin, sizeof(ctis_tables_cubin));
-    return v;
-  }();
-  return img.data();
+// Byte offset and size of the ".nv.constant3" section (the c_tab bank) in the embedded cubin.
+bool constant_bank_section(const unsigned char* img, size_t len, size_t& off, size_t& size) {
+  if (len < 64 || std::memcmp(img, "\x7f" "ELF", 4) != 0 || img[4] != 2) return false;  // ELF64 only
+  uint64_t shoff;
+  uint16_t shentsize, shnum, shstrndx;
+  std::memcpy(&shoff, img + 0x28, 8);
+  std::memcpy(&shentsize, img + 0x3a, 2);
+  std::memcpy(&shnum, img + 0x3c, 2);
+  std::memcpy(&shstrndx, img + 0x3e, 2);
+  if (shoff + (uint64_t)shnum * shentsize > len || shstrndx >= shnum) return false;
+  auto sec = [&](int i, uint32_t& name, uint32_t& type, uint64_t& o, uint64_t& sz) {
+    const unsigned char* h = img + shoff + (uint64_t)i * shentsize;
+    std::memcpy(&name, h + 0, 4);
+    std::memcpy(&type, h + 4, 4);
+    std::memcpy(&o, h + 0x18, 8);
+    std::memcpy(&sz, h + 0x20, 8);
+  };
+  uint32_t n0, t0;
+  uint64_t stro, strsz;
+  sec(shstrndx, n0, t0, stro, strsz);
+  for (int i = 0; i < shnum; ++i) {
+    uint32_t nm, ty;
+    uint64_t o, sz;
+    sec(i, nm, ty, o, sz);
+    if (nm >= strsz || stro + nm >= len) continue;
+    const char* name = reinterpret_cast<const char*>(img + stro + nm);
+    if (ty == 1 /* PROGBITS */ && std::strcmp(name, ".nv.constant3") == 0 && o + sz <= len) {
+      off = (size_t)o;
+      size = (size_t)sz;
+      return true;
+    }
+  }
+  return false;
 }
 
+// Load one instance of the table-kernel cubin whose c_tab bank is initialised with this page:
+// the words are patched into the image's .nv.constant3 section before cudaLibraryLoadData, so the
+// driver itself initialises the bank at module load (lazy or eager).  Writing the bank afterwards
+// with cudaMemcpy was not reliably seen by the first launches of a fresh plan (stale constant data
+// under lazy module loading: tests/test_gpu_parity.py::test_mlem_random_wrapping flaked after a C4 run).
 ctis_status load_page(Page& pg, bool vec) {
-  CTIS_CUDA(cudaLibraryLoadData(&pg.lib, tables_image(), nullptr, nullptr, 0, nullptr, nullptr, 0),
+  const size_t bytes = (size_t)(ctis_tables_cubin_end - ctis_tables_cubin);
+  size_t off = 0, size = 0;
+  if (!constant_bank_section(ctis_tables_cubin, bytes, off, size) || size < (size_t)kPageWords * 4)
+    return fail(CTIS_ERR_CUDA, "embedded cubin: no .nv.constant3 bank for the tap page");
+  if (pg.words.size() > (size_t)kPageWords) return fail(CTIS_ERR_INVALID_ARGUMENT, "tap page overflow");
+  std::vector<uint64_t> img((bytes + 7) / 8, 0);
+  std::memcpy(img.data(), ctis_tables_cubin, bytes);
+  unsigned char* bank = reinterpret_cast<unsigned char*>(img.data()) + off;
+  std::memset(bank, 0, (size_t)kPageWords * 4);
+  std::memcpy(bank, pg.words.data(), pg.words.size() * 4);
+  CTIS_CUDA(cudaLibraryLoadData(&pg.lib, img.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
             "cudaLibraryLoadData (tap page)");
-  void* dptr = nullptr;
-  size_t bytes = 0;
-  CTIS_CUDA(cudaLibraryGetGlobal(&dptr, &bytes, pg.lib, "c_tab"), "cudaLibraryGetGlobal(c_tab)");
-  if (pg.words.size() * 4 > bytes) return fail(CTIS_ERR_INVALID_ARGUMENT, "tap page overflow");
-  CTIS_CUDA(cudaMemcpy(dptr, pg.words.data(), pg.words.size() * 4, cudaMemcpyHostToDevice), "upload tap page");
   std::string name;
   if (pg.forward) {
     name = "ctis_fwd_g" + std::to_string(pg.max_modes / 1000) + "_m" + std::to_string(pg.max_modes % 1000) +
@@ -398,7 +436,7 @@ ctis_status load_page(Page& pg, bool vec) {
   int dev = 0;
   CTIS_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
   // deep window pipelines need more than the default 48 KB of dynamic shared memory
-  const int smem_max = pg.forward ? kFwdStages * (kFwdWinFloats * 4 + 16) : kBackStages * (kBackWinFloats * 4 + 16);
+  const int smem_max = 227 * 1024;  // permission only: launches request what their ring needs
   CTIS_CUDA(cudaKernelSetAttributeForDevice(pg.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max, dev),
             "cudaKernelSetAttributeForDevice");
   return CTIS_OK;
@@ -445,11 +483,20 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
   //      (G groups x MAXM modes, MAXM even: modes are paired for FFMA2) and one TMA box per plan
   {
     std::vector<std::vector<Mode>> chunk_modes;
-    std::vector<std::pair<int, int>> chunks = balanced_chunks(P.w, kFwdBands);
+    // TMA plans may use longer chunks with a wider mode span (fewer chunks -> fewer flush atomics):
+    // CTIS_FWD_BANDS / CTIS_FWD_SPAN override the defaults (experiments)
+    int fbands = kFwdBands, fspan = kModeSpanDefault;
+    if (P.tma_f) {
+      fbands = kFwdBandsTma;  // measured at C4: 16/12 -> 85.3 us, 25/16 -> 82.2 us (C3: 23.0 -> 19.0 us)
+      fspan = kModeSpanTma;
+      if (const char* e = std::getenv("CTIS_FWD_BANDS")) fbands = std::max(1, std::atoi(e));
+      if (const char* e = std::getenv("CTIS_FWD_SPAN")) fspan = std::max(1, std::min(kModeSpanMax, std::atoi(e)));
+    }
+    std::vector<std::pair<int, int>> chunks = balanced_chunks(P.w, fbands);
     int nm_max = 1;
     for (auto [b0, nb] : chunks) {
       std::vector<std::vector<TapXY>> cb(bands.begin() + b0, bands.begin() + b0 + nb);
-      chunk_modes.push_back(cluster_modes(cb));
+      chunk_modes.push_back(cluster_modes(cb, fspan));
       nm_max = std::max(nm_max, (int)chunk_modes.back().size());
     }
     // <= 64 modes: two 16-warp groups split the modes (MAXM per group, multiple of 4, <= 32, keeps
@@ -458,15 +505,39 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     // 512-thread CTAs per SM, one per pass (G = 1, default: a CTA's prologue, first-window latency
     // and flush overlap the other CTA's tap loop; measured 78 vs 95 us at C4), or as one 1024-thread
     // CTA with two mode groups sharing each window (G = 2; CTIS_FWD_GROUPS=2).
-    if (nm_max <= 64) {
-      P.fwd_g = 1;
-      P.fwd_m = std::max(2, ((nm_max + 1) / 2 + 1) / 2 * 2);
+    // Default (TMA plans): forward_persistent2 — two u positions per thread, passes of <= 32 modes
+    // (CTIS_FWD_MAXM overrides the cap; templates: even MAXM <= 32, 36, 40).  CTIS_FWD_POS=1 selects
+    // the one-position kernel (forward_persistent / forward_body; also used by element-loader plans).
+    const char* pos_env = std::getenv("CTIS_FWD_POS");
+    const bool two_pos = P.tma_f && !(pos_env && std::atoi(pos_env) == 1);
+    int maxm;
+    if (two_pos) {
+      const char* cap_env = std::getenv("CTIS_FWD_MAXM");
+      const int cap = cap_env ? std::max(2, std::min(40, std::atoi(cap_env))) : 32;
+      const int npass = (nm_max + cap - 1) / cap;
+      int mm = std::max(2, ((nm_max + npass - 1) / npass + 1) / 2 * 2);
+      if (mm > 32) mm = mm <= 36 ? 36 : 40;
+      // CTAs per SM (256 threads each): 2 (8-stage ring, <= 128 registers), 3 (6 stages, MAXM <= 24),
+      // 4 (4 stages, MAXM <= 16)
+      const char* occ_env = std::getenv("CTIS_FWD_OCC");
+      int occ = occ_env ? std::atoi(occ_env) : 2;
+      if (occ == 4 && mm > 16) occ = 3;
+      if (occ == 3 && mm > 24) occ = 2;
+      if (occ < 2 || occ > 4) occ = 2;
+      P.fwd_g = occ;
+      P.fwd_m = mm;
+      maxm = mm;
     } else {
-      P.fwd_g = 1;
-      P.fwd_m = std::max(40, std::min(96, (nm_max + 7) / 8 * 8));
+      if (nm_max <= 64) {
+        P.fwd_g = 1;
+        P.fwd_m = std::max(2, ((nm_max + 1) / 2 + 1) / 2 * 2);
+      } else {
+        P.fwd_g = 1;
+        P.fwd_m = std::max(40, std::min(96, (nm_max + 7) / 8 * 8));
+      }
+      // modes per pass (G = 1 with a small MAXM: two passes of MAXM modes)
+      maxm = (P.fwd_g == 1 && P.fwd_m <= 32) ? P.fwd_m : P.fwd_g * P.fwd_m;
     }
-    // modes per pass (G = 1 with a small MAXM: two passes of MAXM modes)
-    const int maxm = (P.fwd_g == 1 && P.fwd_m <= 32) ? P.fwd_m : P.fwd_g * P.fwd_m;
     std::vector<std::vector<const Mode*>> passes;
     std::vector<int> pass_chunk;
     for (size_t k = 0; k < chunk_modes.size(); ++k)
@@ -682,6 +753,14 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
     delete p;
     return fail(st, msg);
   }
+  // The tap pages and h were uploaded with cudaMemcpy from pageable memory, which may return before
+  // the DMA lands; kernels run on caller / side streams that need not order after the legacy stream.
+  // Wait here so that the plan is complete when ctis_plan_create returns.
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    delete p;
+    return cuda_fail(e, "plan upload");
+  }
   *out = p;
   g_last_error.clear();
   return CTIS_OK;
@@ -767,7 +846,7 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
   const int nsub = (int)((bias + emax + P.n - 1) / P.n);
   const int box_r = fwd ? P.fbox_r : P.bbox_r, box_c = fwd ? P.fbox_c : P.bbox_c;
   const int cap = fwd ? kFwdWinFloats : kBackWinFloats;
-  const int slot = tma ? (box_r * box_c + 31) / 32 * 32 : cap;
+  int slot = tma ? (box_r * box_c + 31) / 32 * 32 : cap;
   TabArgs A{src, dst, src_frame, dst_frame, P.a, P.alpha, P.gamma, P.xi, P.n, P.ell, mode, bias, nsub,
             slot, box_r, box_c, (unsigned)(4 * box_r * box_c), debug_flags(), frames};
   alignas(64) CUtensorMap tm;
@@ -776,15 +855,16 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
     cudaError_t e = make_tensor_map(&tm, fwd, P, src, frames);
     if (e != cudaSuccess) return e;
   }
-  const int threads = fwd ? P.fwd_g * kFwdThreads : kBackThreads;
-  const int stages = fwd ? kFwdStages : kBackStages;
+  const int threads = fwd ? (P.fwd_g >= 2 ? kFwd2Threads : kFwdThreads) : kBackThreads;
+  const int stages = fwd ? (P.fwd_g == 3 ? 6 : P.fwd_g == 4 ? 4 : kFwdStages) : kBackStages;
   const size_t smem = (size_t)stages * slot * sizeof(float) + 16 * stages;  // + full/empty mbarriers
   A.frames = frames;
   for (const Page& pg : pages) {
     // TMA kernels are persistent (2 CTAs per SM walk the page's items); element-loader kernels are
     // one CTA per (tile, chunk, frame)
     const long long items = (long long)pg.total_items * frames;
-    dim3 grid = tma ? dim3((unsigned)std::min<long long>(items, 2LL * P.sms), 1, 1)
+    const int per_sm = (fwd && P.fwd_g >= 2) ? P.fwd_g : 2;
+    dim3 grid = tma ? dim3((unsigned)std::min<long long>(items, (long long)per_sm * P.sms), 1, 1)
                     : dim3(pg.max_tiles, pg.nchunks, frames);
     void* args[] = {&A, &tm};
     cudaError_t e = cudaLaunchKernel((const void*)pg.kern, grid, dim3(threads), args, smem, s);

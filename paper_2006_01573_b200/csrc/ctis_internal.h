@@ -39,7 +39,8 @@ enum : int { kDescHeader = 8, kItemBase = 64, kPageHeaderWords = 128 };
 constexpr int kFwdTR = 32;
 constexpr int kFwdTC = 16;
 constexpr int kFwdThreads = kFwdTR * kFwdTC;   // per group
-constexpr int kFwdBands = 16;           // max bands per forward chunk (chunks are balanced)
+constexpr int kFwd2Threads = kFwdThreads / 2;  // two u positions per thread (forward_persistent2)
+constexpr int kFwdBands = 16;           // default max bands per forward chunk (chunks are balanced)
 // Back kernel geometry: 32 x 32 voxel tile, 2 voxels per thread, NB in {4, 8, 12, 16} bands
 // per chunk (kernel template; the plan picks the one that fills the 148 SMs best).
 constexpr int kBackTR = 32;
@@ -47,12 +48,18 @@ constexpr int kBackTC = 32;
 constexpr int kBackThreads = 512;
 constexpr int kBackBandsMax = 16;
 
-// Mode shifts are bounded by kModeSpan (|dr|, |dc| <= 12 from the mode reference), so a window
-// never exceeds (32 + 24 + 3 -> 60) x (16 + 24) floats (forward) or 60 x (32 + 24) (back).
-constexpr int kModeSpanMax = 12;
+// Mode shifts are bounded by the plan's span (|dr|, |dc| <= span from the mode reference; default
+// kModeSpanDefault, at most kModeSpanMax), so an element-loader window never exceeds
+// (32 + 2*span) x (16 + 2*span) floats (forward) or (32 + 2*span) x (32 + 2*span) (back).
+constexpr int kModeSpanDefault = 12;
+constexpr int kModeSpanMax = 32;
+// TMA forward plans: longer chunks with a wider mode span (fewer chunks -> fewer flush atomics)
+constexpr int kFwdBandsTma = 25;
+constexpr int kModeSpanTma = 16;
 constexpr int kFwdStages = 8;           // window pipeline depth (TMA boxes / cp.async groups in flight),
 constexpr int kBackStages = 8;          // refilled K = stages/2 at a time
-constexpr int kFwdWinFloats = 2560;     // 10 KB per stage (>= 60 x 40)
+constexpr int kFwdWinFloats = 2560;     // element-loader slot: 10 KB per stage (>= 56 x 40)
+constexpr int kTmaWinFloats = 8192;     // TMA box cap (32 KB)
 constexpr int kBackWinFloats = 3584;    // 14 KB per stage (>= 60 x 56)
 
 // Per-launch parameters of the table kernels.

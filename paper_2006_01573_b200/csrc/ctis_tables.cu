@@ -42,8 +42,14 @@ __device__ __forceinline__ const uint4* tab4(uint32_t word4) {
 
 namespace {
 
-__device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool valid) {
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool valid, bool cg = false) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if (cg) {  // experiment: L1-bypassing synchronous load
+    float v = 0.f;
+    if (valid) asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(gmem) : "memory");
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(s), "f"(v) : "memory");
+    return;
+  }
   const int sz = valid ? 4 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
 }
@@ -121,7 +127,7 @@ __device__ __forceinline__ void load_f_window(float* buf, const float* fl, const
     for (int i = lane; i < WR; i += 32) {
       const int rr = row0 + i;
       const bool ok = cok & (rr >= 0) & (rr < A.a);
-      cp_async4(buf + i + WR * j, ok ? fl + rr + A.a * cc : fl, ok);
+      cp_async4(buf + i + WR * j, ok ? fl + rr + A.a * cc : fl, ok, A.dbg & 4);
     }
   }
 }
@@ -138,7 +144,7 @@ __device__ __forceinline__ void load_r_window(float* buf, const float* r, const 
     for (int i = lane; i < WR; i += 32) {
       unsigned idx = cb + (unsigned)i;
       while (idx >= n) idx -= n;
-      cp_async4(buf + i + WR * j, r + idx, true);
+      cp_async4(buf + i + WR * j, r + idx, true, A.dbg & 4);
     }
   }
 }
@@ -267,7 +273,9 @@ __device__ __forceinline__ void forward_group(const TabArgs& A, const CUtensorMa
       issue(b + S - 1);
       cp_wait<S - 1>();
       __syncthreads();
-      compute(sbase + 4u * ((b % S) * A.slot_floats + lane + tabi(BI + 4 * b + 2) * warp), b);
+      // a band without taps in this pass has an empty window (WC = 0): nothing was loaded into its
+      // slot, so it must not be read (stale shared memory may hold NaN/Inf, and 0 * NaN != 0)
+      if (tabi(BI + 4 * b + 3) != 0) compute(sbase + 4u * ((b % S) * A.slot_floats + lane + tabi(BI + 4 * b + 2) * warp), b);
       __syncthreads();  // every thread is done with this slot before it is refilled
     }
   }
@@ -609,6 +617,146 @@ __device__ __forceinline__ void forward_persistent(const TabArgs& A, const CUten
   }
 }
 
+
+// Forward, two u positions per thread (columns warp and warp + 8 of a 32 x 16 tile; 256 threads):
+// every tap entry read through the uniform datapath (LDCU.64) feeds four shared-memory loads and two
+// FFMA2, halving the table and loop-control instructions per tap of forward_persistent (the kernel
+// is issue-bound, not shared-memory-bound, with one position per thread: ncu r01c).  The flush is
+// branch-free (predicated red.global.add per mode and position).
+__device__ __forceinline__ void red_nz(float* p, float v) {
+  asm volatile(
+      "{\n.reg .pred q;\n"
+      "setp.ne.f32 q, %1, 0f00000000;\n"
+      "@q red.global.add.f32 [%0], %1;\n}\n" ::"l"(p),
+      "f"(v)
+      : "memory");
+}
+
+template <int MAXM, int S>
+__device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUtensorMap* tm) {
+  extern __shared__ __align__(128) float smem[];
+  constexpr int K = S / 2, MP = MAXM / 2;
+  constexpr int NW = kFwd2Threads / 32;  // 8 warps; warp w owns columns w and w + NW
+  static_assert(2 * NW == kFwdTC, "two columns per warp");
+  const int nch = tabi(0);
+  const int per_frame = tabi(kItemBase + nch);
+  const int items = per_frame * A.frames;
+  if ((int)blockIdx.x >= items) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned slot_bytes = 4u * A.slot_floats;
+  const unsigned full = sbase + S * slot_bytes;
+
+  int p_item = blockIdx.x, p_band = 0, p_nb = 0, p_z = 0, p_Ur = 0, p_Uc = 0, p_lam0 = 0;
+  uint32_t p_BI = 0;
+  unsigned p_w = 0;
+  auto p_load_item = [&]() {
+    int k, tile;
+    decode_item(p_item, per_frame, nch, p_z, k, tile);
+    const uint32_t D = c_tab[1 + k];
+    const int tiles_r = tabi(D + 5), nm = tabi(D + 2);
+    p_lam0 = tabi(D + 0);
+    p_nb = tabi(D + 1);
+    p_Ur = tabi(D + 3) + (tile % tiles_r) * kFwdTR;
+    p_Uc = tabi(D + 4) + (tile / tiles_r) * kFwdTC;
+    p_BI = D + kDescHeader + ((nm + 3) & ~3);
+    p_band = 0;
+  };
+  unsigned p_slot = 0;
+  auto issue_one = [&]() {
+    if (p_item >= items) return;
+    const uint32_t bi = p_BI + 4 * p_band;
+    mbar_expect_tx(full + 8 * p_slot, A.box_bytes);
+    tma_4d(sbase + p_slot * slot_bytes, tm, p_Ur + tabi(bi + 0), p_Uc + tabi(bi + 1), p_lam0 + p_band, p_z,
+           full + 8 * p_slot);
+    ++p_w;
+    if (++p_slot == S) p_slot = 0;
+    if (++p_band == p_nb) {
+      p_item += gridDim.x;
+      if (p_item < items) p_load_item();
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(full + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    p_load_item();
+    if (!(A.dbg & 1)) {
+#pragma unroll 1
+      for (int s = 0; s < S; ++s) issue_one();
+    }
+  }
+  __syncthreads();
+
+  unsigned c_slot = 0, c_phase = 0;  // consumer position in the ring
+  const unsigned tb0 = sbase + 4u * (lane + A.box_r * warp);
+  const unsigned tb1 = tb0 + 4u * A.box_r * NW;
+  const unsigned n = (unsigned)A.n;
+  unsigned w = 0, next_refill = K;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    int z, k, tile;
+    decode_item(it, per_frame, nch, z, k, tile);
+    const uint32_t D = c_tab[1 + k];
+    const int nb = tabi(D + 1), nm = tabi(D + 2), tiles_r = tabi(D + 5);
+    const int U_r = tabi(D + 3) + (tile % tiles_r) * kFwdTR, U_c = tabi(D + 4) + (tile / tiles_r) * kFwdTC;
+    const uint32_t TP = D + kDescHeader + ((nm + 3) & ~3) + 4 * nb;
+    float2 a0[MP], a1[MP];
+#pragma unroll
+    for (int q = 0; q < MP; ++q) a0[q] = a1[q] = make_float2(0.f, 0.f);
+    auto compute = [&](unsigned off, int b) {
+      const uint4* ent = tab4(TP) + b * MP;
+#pragma unroll
+      for (int q = 0; q < MP; ++q) {
+        const uint4 e = ent[q];
+        const float2 wv = make_float2(__uint_as_float(e.z), __uint_as_float(e.w));
+        a0[q] = __ffma2_rn(wv, make_float2(lds(tb0 + off + e.x), lds(tb0 + off + e.y)), a0[q]);
+        a1[q] = __ffma2_rn(wv, make_float2(lds(tb1 + off + e.x), lds(tb1 + off + e.y)), a1[q]);
+      }
+    };
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b, ++w) {
+      if (w >= next_refill) {
+        __syncthreads();  // every warp has consumed the windows before w: their slots are free
+        if (threadIdx.x == 0 && !(A.dbg & 1)) {
+#pragma unroll 1
+          for (int q = 0; q < K; ++q)
+            if (p_w < w + S) issue_one();
+        }
+        next_refill = w + K;
+      }
+      if (!(A.dbg & 1)) mbar_wait(full + 8 * c_slot, c_phase);
+      compute(c_slot * slot_bytes, b);
+      if (++c_slot == S) {
+        c_slot = 0;
+        c_phase ^= 1u;
+      }
+    }
+    // flush this item: g_hat[(E(u) + o_ref) mod n] += acc for both positions (see forward_group)
+    float* g = A.dst + (long long)z * A.dst_frame;
+    if (A.dbg & 2) {  // profiling: no flush (keep the accumulators live)
+      float t = 0.f;
+#pragma unroll
+      for (int q = 0; q < MP; ++q) t += a0[q].x + a0[q].y + a1[q].x + a1[q].y;
+      if (t == -1.f) g[0] = t;
+      continue;
+    }
+    unsigned ub0 = (unsigned)((U_r + lane) + A.gamma * (U_c + warp)) + A.bias;
+    for (int q = 0; q < A.nsub; ++q) ub0 = min(ub0, ub0 - n);
+    unsigned ub1 = ub0 + (unsigned)(((unsigned long long)A.gamma * NW) % n);  // E(u + NW columns) mod n
+    ub1 = min(ub1, ub1 - n);
+#pragma unroll
+    for (int c = 0; c < MAXM; ++c) {
+      if (c < nm) {
+        const unsigned o = c_tab[D + kDescHeader + c];
+        unsigned P0 = ub0 + o, P1 = ub1 + o;
+        P0 = min(P0, P0 - n);
+        P1 = min(P1, P1 - n);
+        red_nz(g + P0, (c & 1) ? a0[c >> 1].y : a0[c >> 1].x);
+        red_nz(g + P1, (c & 1) ? a1[c >> 1].y : a1[c >> 1].x);
+      }
+    }
+  }
+}
+
 template <int NB>
 __device__ __forceinline__ void back_persistent(const TabArgs& A, const CUtensorMap* tm) {
   extern __shared__ __align__(128) float smem[];
@@ -741,15 +889,27 @@ __device__ __forceinline__ void back_persistent(const TabArgs& A, const CUtensor
   }
 }
 
+// CTIS_DEBUG & 8: fill the window ring with NaN before the kernel runs, so that any read of shared
+// memory the kernel did not write this launch poisons the result (tests/test_gpu_parity.py)
+__device__ __forceinline__ void nan_fill_smem(int nf) {
+  extern __shared__ __align__(128) float smem[];
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) smem[i] = __int_as_float(0x7fc00000);
+  __syncthreads();
+}
+
 }  // namespace
 
 #define CTIS_FWD(M, MINB)                                                                                  \
   extern "C" __global__ void __launch_bounds__(kFwdThreads, MINB)                                          \
       ctis_fwd_g1_m##M##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                      \
+    if (A.frames == 0) return;                                                                             \
+    if (A.dbg & 8) nan_fill_smem(kFwdStages * A.slot_floats);                                                  \
     forward_persistent<M>(A, &tm);                                                                         \
   }                                                                                                        \
   extern "C" __global__ void __launch_bounds__(kFwdThreads, MINB)                                          \
       ctis_fwd_g1_m##M##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                      \
+    if (A.frames == 0) return;                                                                             \
+    if (A.dbg & 8) nan_fill_smem(kFwdStages * A.slot_floats);                                                  \
     forward_body<1, M, false, true>(A, &tm);                                                               \
   }
 CTIS_FWD(2, 2)
@@ -777,13 +937,63 @@ CTIS_FWD(80, 1)
 CTIS_FWD(88, 1)
 CTIS_FWD(96, 1)
 
+#define CTIS_FWD2(OCC, S, M)                                                                               \
+  extern "C" __global__ void __launch_bounds__(kFwd2Threads, OCC)                                          \
+      ctis_fwd_g##OCC##_m##M##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                \
+    if (A.frames == 0) return;                                                                             \
+    if (A.dbg & 8) nan_fill_smem(S * A.slot_floats);                                                           \
+    forward_persistent2<M, S>(A, &tm);                                                                     \
+  }
+CTIS_FWD2(2, 8, 2)
+CTIS_FWD2(2, 8, 4)
+CTIS_FWD2(2, 8, 6)
+CTIS_FWD2(2, 8, 8)
+CTIS_FWD2(2, 8, 10)
+CTIS_FWD2(2, 8, 12)
+CTIS_FWD2(2, 8, 14)
+CTIS_FWD2(2, 8, 16)
+CTIS_FWD2(2, 8, 18)
+CTIS_FWD2(2, 8, 20)
+CTIS_FWD2(2, 8, 22)
+CTIS_FWD2(2, 8, 24)
+CTIS_FWD2(2, 8, 26)
+CTIS_FWD2(2, 8, 28)
+CTIS_FWD2(2, 8, 30)
+CTIS_FWD2(2, 8, 32)
+CTIS_FWD2(2, 8, 36)
+CTIS_FWD2(2, 8, 40)
+CTIS_FWD2(3, 6, 2)
+CTIS_FWD2(3, 6, 4)
+CTIS_FWD2(3, 6, 6)
+CTIS_FWD2(3, 6, 8)
+CTIS_FWD2(3, 6, 10)
+CTIS_FWD2(3, 6, 12)
+CTIS_FWD2(3, 6, 14)
+CTIS_FWD2(3, 6, 16)
+CTIS_FWD2(3, 6, 18)
+CTIS_FWD2(3, 6, 20)
+CTIS_FWD2(3, 6, 22)
+CTIS_FWD2(3, 6, 24)
+CTIS_FWD2(4, 4, 2)
+CTIS_FWD2(4, 4, 4)
+CTIS_FWD2(4, 4, 6)
+CTIS_FWD2(4, 4, 8)
+CTIS_FWD2(4, 4, 10)
+CTIS_FWD2(4, 4, 12)
+CTIS_FWD2(4, 4, 14)
+CTIS_FWD2(4, 4, 16)
+
 #define CTIS_BACK(NB)                                                                                      \
   extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
       ctis_back_b##NB##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                       \
-    back_persistent<NB>(A, &tm);                                                                           \
+    if (A.frames == 0) return;                                                                             \
+    if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                                 \
+    back_persistent<NB>(A, &tm);                                                                     \
   }                                                                                                        \
   extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
       ctis_back_b##NB##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                       \
+    if (A.frames == 0) return;                                                                             \
+    if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                                 \
     back_body<NB, false, true>(A, &tm);                                                                    \
   }
 CTIS_BACK(4)

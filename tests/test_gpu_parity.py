@@ -282,3 +282,16 @@ def test_error_codes(ctis, dev):
     with pytest.raises(ctis.CtisError) as ei:
         plan.mlem(torch.ones(geom.n, device=dev), torch.ones(geom.m, device=dev), -1)
     assert ei.value.status == ctis.ERR_INVALID_ARGUMENT
+
+
+def test_no_stale_shared_memory_reads(ctis):
+    """Every projection kernel with CTIS_DEBUG=8 NaN-fills its window ring first: results must not
+    change (a band without taps in a forward pass once read a slot it never loaded)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, CTIS_DEBUG="8")
+    r = subprocess.run([sys.executable, os.path.join(here, "poison_case.py")], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -14,10 +14,12 @@ fu = torch.ones(cfg.geom.m, device="cuda")
 out = {}
 for nm, fn in (("forward", lambda: plan.forward_accumulate(f, g)), ("back", lambda: plan.back_update(r, fu))):
     for _ in range(3): fn()
-    ts = []
-    for _ in range(20):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(); fn(); b.record(); ts.append((a, b))
     torch.cuda.synchronize()
-    out[nm] = statistics.median(x.elapsed_time(y) for x, y in ts) * 1e3
+    # 30 back-to-back launches between two events: the host runs ahead, so the average is device time
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(30): fn()
+    b.record()
+    torch.cuda.synchronize()
+    out[nm] = a.elapsed_time(b) / 30 * 1e3
 print(name, "dbg=%s" % os.environ.get("CTIS_DEBUG", "0"), " ".join(f"{k}={v:.1f}us" for k, v in out.items()))
