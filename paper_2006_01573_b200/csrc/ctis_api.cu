@@ -412,6 +412,15 @@ bool constant_bank_section(const unsigned char* img, size_t len, size_t& off, si
 // driver itself initialises the bank at module load (lazy or eager).  Writing the bank afterwards
 // with cudaMemcpy was not reliably seen by the first launches of a fresh plan (stale constant data
 // under lazy module loading: tests/test_gpu_parity.py::test_mlem_random_wrapping flaked after a C4 run).
+// TMA back kernel with four voxels per thread (256 threads); CTIS_BACK4=0 selects the 512-thread one
+bool back4_enabled() {
+  static bool v = [] {
+    const char* e = std::getenv("CTIS_BACK4");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return v;
+}
+
 ctis_status load_page(Page& pg, bool vec) {
   const size_t bytes = (size_t)(ctis_tables_cubin_end - ctis_tables_cubin);
   size_t off = 0, size = 0;
@@ -430,7 +439,8 @@ ctis_status load_page(Page& pg, bool vec) {
     name = "ctis_fwd_g" + std::to_string(pg.max_modes / 1000) + "_m" + std::to_string(pg.max_modes % 1000) +
            (vec ? "_t" : "_s");
   } else {
-    name = "ctis_back_b" + std::to_string(pg.max_modes) + (vec ? "_t" : "_s");
+    name = std::string(vec && back4_enabled() ? "ctis_back4_b" : "ctis_back_b") + std::to_string(pg.max_modes) +
+           (vec ? "_t" : "_s");
   }
   CTIS_CUDA(cudaLibraryGetKernel(&pg.kern, pg.lib, name.c_str()), "cudaLibraryGetKernel");
   int dev = 0;
@@ -457,6 +467,10 @@ std::vector<std::pair<int, int>> balanced_chunks(int w, int maxb) {
 
 // Back-kernel band template: minimise (waves over 2 CTAs/SM) x (NB + window cost in band units).
 int choose_back_nb(const ctis_plan_s& P) {
+  if (const char* e = std::getenv("CTIS_BACK_NB")) {  // experiments: 4, 8, 12 or 16
+    const int v = std::atoi(e);
+    if (v == 4 || v == 8 || v == 12 || v == 16) return v;
+  }
   const long long tiles = (long long)((P.a + kBackTR - 1) / kBackTR) * ((P.alpha + kBackTC - 1) / kBackTC);
   const long long slots = 148LL * 2;
   int best = kBackBandsMax;
@@ -855,7 +869,7 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
     cudaError_t e = make_tensor_map(&tm, fwd, P, src, frames);
     if (e != cudaSuccess) return e;
   }
-  const int threads = fwd ? (P.fwd_g >= 2 ? kFwd2Threads : kFwdThreads) : kBackThreads;
+  const int threads = fwd ? (P.fwd_g >= 2 ? kFwd2Threads : kFwdThreads) : (tma && back4_enabled() ? kBack4Threads : kBackThreads);
   const int stages = fwd ? (P.fwd_g == 3 ? 6 : P.fwd_g == 4 ? 4 : kFwdStages) : kBackStages;
   const size_t smem = (size_t)stages * slot * sizeof(float) + 16 * stages;  // + full/empty mbarriers
   A.frames = frames;

@@ -46,6 +46,7 @@ constexpr int kFwdBands = 16;           // default max bands per forward chunk (
 constexpr int kBackTR = 32;
 constexpr int kBackTC = 32;
 constexpr int kBackThreads = 512;
+constexpr int kBack4Threads = 256;  // back_persistent4: four voxels per thread
 constexpr int kBackBandsMax = 16;
 
 // Mode shifts are bounded by the plan's span (|dr|, |dc| <= span from the mode reference; default

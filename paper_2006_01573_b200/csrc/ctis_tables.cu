@@ -897,6 +897,147 @@ __device__ __forceinline__ void nan_fill_smem(int nf) {
   __syncthreads();
 }
 
+// Back with four voxels per thread (columns warp + 8k of the 32 x 32 tile, 256 threads): every tap
+// entry read through the uniform datapath feeds eight shared-memory loads (cf. forward_persistent2).
+template <int NB>
+__device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtensorMap* tm) {
+  extern __shared__ __align__(128) float smem[];
+  constexpr int S = kBackStages, K = S / 2, BP = NB / 2;
+  constexpr int NWARPS = kBack4Threads / 32;  // 8: voxel columns warp + 8k, k < 4
+  const int nch = tabi(0);
+  const int per_frame = tabi(kItemBase + nch);
+  const int items = per_frame * A.frames;
+  if ((int)blockIdx.x >= items) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned slot_bytes = 4u * A.slot_floats;
+  const unsigned full = sbase + S * slot_bytes;
+
+  // window origin of mode c of the tile at (q_r0, q_c0): host-split Bm = Bm_r + gamma*Bm_c, one carry
+  // and one wrap (the plan only selects this kernel when no window of the page wraps)
+  auto origin_rc = [&](uint32_t MI, int c, int q_r0, int q_c0, int& R0, int& C0) {
+    R0 = q_r0 + tabi(MI + 4 * c + 0);
+    C0 = q_c0 + tabi(MI + 4 * c + 1);
+    if (R0 >= A.gamma) {
+      R0 -= A.gamma;
+      C0 += 1;
+    }
+    if (C0 >= A.xi) C0 -= A.xi;
+  };
+  int p_item = blockIdx.x, p_mode = 0, p_nm = 0, p_z = 0, p_qr = 0, p_qc = 0;
+  uint32_t p_MI = 0;
+  unsigned p_w = 0;
+  auto p_load_item = [&]() {
+    int k, tile;
+    decode_item(p_item, per_frame, nch, p_z, k, tile);
+    const uint32_t D = c_tab[1 + k];
+    const int tiles_r = tabi(D + 3);
+    p_nm = tabi(D + 2);
+    p_qr = (tile % tiles_r) * kBackTR;
+    p_qc = (tile / tiles_r) * kBackTC;
+    p_MI = D + kDescHeader;
+    p_mode = 0;
+  };
+  auto issue_one = [&]() {
+    if (p_item >= items) return;
+    const unsigned slot = p_w & (S - 1);
+    int R0, C0;
+    origin_rc(p_MI, p_mode, p_qr, p_qc, R0, C0);
+    mbar_expect_tx(full + 8 * slot, A.box_bytes);
+    tma_3d(sbase + slot * slot_bytes, tm, R0, C0, p_z, full + 8 * slot);
+    ++p_w;
+    if (++p_mode == p_nm) {
+      p_item += gridDim.x;
+      if (p_item < items) p_load_item();
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < S; ++q) mbar_init(full + 8 * q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    p_load_item();
+#pragma unroll
+    for (int q = 0; q < S; ++q) issue_one();
+  }
+  __syncthreads();
+
+  const unsigned t0 = sbase + 4u * (lane + A.box_r * warp), cstep = 4u * A.box_r * NWARPS;
+  unsigned w = 0, next_refill = K;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    int z, k, tile;
+    decode_item(it, per_frame, nch, z, k, tile);
+    const uint32_t D = c_tab[1 + k];
+    const int lam0 = tabi(D + 0), nb = tabi(D + 1), nm = tabi(D + 2), tiles_r = tabi(D + 3);
+    const int q_r0 = (tile % tiles_r) * kBackTR, q_c0 = (tile / tiles_r) * kBackTC;
+    const uint32_t MI = D + kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * NB;
+    float2 acc[4][BP];
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4)
+#pragma unroll
+      for (int q = 0; q < BP; ++q) acc[k4][q] = make_float2(0.f, 0.f);
+    auto compute = [&](unsigned ba, int c) {
+      const uint4* ent = tab4(TP) + c * BP;
+#pragma unroll
+      for (int q = 0; q < BP; ++q) {
+        const uint4 e = ent[q];
+        const float2 wv = make_float2(__uint_as_float(e.z), __uint_as_float(e.w));
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const unsigned bk = ba + k4 * cstep;
+          acc[k4][q] = __ffma2_rn(wv, make_float2(lds(bk + e.x), lds(bk + e.y)), acc[k4][q]);
+        }
+      }
+    };
+    for (int c = 0; c < nm;) {
+      if (w >= next_refill) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+#pragma unroll
+          for (int q = 0; q < K; ++q)
+            if (p_w < w + S) issue_one();
+        }
+        next_refill = w + K;
+      }
+      const unsigned s0 = w & (S - 1);
+      mbar_wait(full + 8 * s0, (w / S) & 1u);
+      compute(t0 + s0 * slot_bytes, c);
+      if (c + 1 < nm) {
+        const unsigned s1 = (w + 1) & (S - 1);
+        mbar_wait(full + 8 * s1, ((w + 1) / S) & 1u);
+        compute(t0 + s1 * slot_bytes, c + 1);
+        w += 2;
+        c += 2;
+      } else {
+        w += 1;
+        c += 1;
+      }
+    }
+    // epilogue of this item: f <- f * z * (1/h_lam) (or z); all loads of f first, then the stores
+    float* f = A.dst + (long long)z * A.dst_frame;
+    const int qr = q_r0 + lane;
+    if (qr < A.a) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (b < nb) {
+          const long long lb = (long long)(lam0 + b) * A.ell + qr;
+          const float ih = tabf(IH + b);
+          float old[4];
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int qc = q_c0 + warp + NWARPS * k4;
+            old[k4] = (A.mode && qc < A.alpha) ? f[lb + (long long)A.a * qc] : 1.f;
+          }
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int qc = q_c0 + warp + NWARPS * k4;
+            const float zz = (b & 1) ? acc[k4][b >> 1].y : acc[k4][b >> 1].x;
+            if (qc < A.alpha) f[lb + (long long)A.a * qc] = A.mode ? old[k4] * zz * ih : zz;
+          }
+        }
+      }
+    }
+  }
+}
+
 }  // namespace
 
 #define CTIS_FWD(M, MINB)                                                                                  \
@@ -982,6 +1123,18 @@ CTIS_FWD2(4, 4, 10)
 CTIS_FWD2(4, 4, 12)
 CTIS_FWD2(4, 4, 14)
 CTIS_FWD2(4, 4, 16)
+
+#define CTIS_BACK4(NB)                                                                                     \
+  extern "C" __global__ void __launch_bounds__(kBack4Threads, 2)                                           \
+      ctis_back4_b##NB##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                      \
+    if (A.frames == 0) return;                                                                             \
+    if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                             \
+    back_persistent4<NB>(A, &tm);                                                                          \
+  }
+CTIS_BACK4(4)
+CTIS_BACK4(8)
+CTIS_BACK4(12)
+CTIS_BACK4(16)
 
 #define CTIS_BACK(NB)                                                                                      \
   extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
