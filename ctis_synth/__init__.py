@@ -223,3 +223,12 @@ def scene_random(geom: Geometry, seed: int, lo: float = 0.0, hi: float = 1.0,
 def frame_scene(geom: Geometry, frame: int) -> np.ndarray:
     """C5 snapshot-video frame i: scene S1 with seed 1000 + i."""
     return scene_blobs(geom, seed=1000 + frame)
+
+
+def poisson_counts(g: np.ndarray, seed: int, photons: float = 1.0) -> np.ndarray:
+    """Photon-limited measurement: independent Poisson counts with mean photons * g_p, returned as
+    float32 (§8(f) f-3 second workload shape).  Random numbers only: the mean g comes from the caller."""
+    rng = np.random.default_rng(seed)
+    lam = np.asarray(g, np.float64) * float(photons)
+    return rng.poisson(lam).astype(np.float32)
+

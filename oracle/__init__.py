@@ -58,6 +58,10 @@ def _load():
             lib.oracle_sensitivity.argtypes = geo + [P, P, P, P]
             lib.oracle_sensitivity.restype = ctypes.c_int
             lib.oracle_mlem.argtypes = geo + [P, P, P, P, P, i64, P]
+            lib.oracle_loglik.argtypes = [i64, P, P]
+            lib.oracle_loglik.restype = ctypes.c_double
+            lib.oracle_mlem_monitored.argtypes = geo + [P, P, P, P, P, i64, ctypes.c_double, P, P]
+            lib.oracle_mlem_monitored.restype = ctypes.c_int
             lib.oracle_mlem.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -135,3 +139,29 @@ def mlem(geom, taps, g, f0, iters: int, return_ghat: bool = False):
     _check(lib.oracle_mlem(*_geo(geom), _ptr(ptr), _ptr(off), _ptr(wt), _ptr(gd), _ptr(f), int(iters),
                            _ptr(gh) if gh is not None else None), "mlem")
     return (f, gh) if return_ghat else f
+
+
+def loglik(g, ghat) -> float:
+    """Poisson log-likelihood sum_p [g_p log ghat_p - ghat_p] (ctis_oracle.c: oracle_loglik)."""
+    lib = _load()
+    gd = np.ascontiguousarray(np.asarray(g, np.float64).reshape(-1))
+    hd = np.ascontiguousarray(np.asarray(ghat, np.float64).reshape(-1))
+    assert gd.size == hd.size
+    return float(lib.oracle_loglik(gd.size, _ptr(gd), _ptr(hd)))
+
+
+def mlem_monitored(geom, taps, g, f0, max_iters: int, rel_tol: float):
+    """Alg. 1 with the per-iteration log-likelihood and the early stop (oracle_mlem_monitored):
+    returns (f, ll[:iters_done], iters_done)."""
+    lib = _load()
+    ptr, off, wt = _taps(taps)
+    gd = np.ascontiguousarray(np.asarray(g, np.float64).reshape(-1))
+    f = np.array(np.asarray(f0, np.float64).reshape(-1), copy=True)
+    assert gd.size == geom.n and f.size == geom.m
+    ll = np.zeros(max(int(max_iters), 1), np.float64)
+    done = np.zeros(1, np.int64)
+    _check(lib.oracle_mlem_monitored(*_geo(geom), _ptr(ptr), _ptr(off), _ptr(wt), _ptr(gd), _ptr(f),
+                                     int(max_iters), float(rel_tol), _ptr(ll), _ptr(done)), "mlem_monitored")
+    k = int(done[0])
+    return f, ll[:k], k
+

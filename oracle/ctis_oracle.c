@@ -42,6 +42,7 @@
  * Richardson-Lucy for w = 1.
  */
 #include <stdint.h>
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -186,3 +187,49 @@ done:
     free(h); free(gk); free(u); free(zeta);
     return rc;
 }
+
+/* Poisson log-likelihood of the measurement g under the model ghat = H f, without the
+ * f-independent -log(g_p!) term: L = sum_p [ g_p log ghat_p - ghat_p ] (the objective MLEM
+ * ascends, Shepp & Vardi, cited at PAPER.md P:34).  Pixels with ghat_p <= 0 contribute 0 when
+ * g_p = 0 and -infinity otherwise (reading R15).  Sum in ascending p. */
+double oracle_loglik(int64_t n, const double* g, const double* ghat) {
+    double L = 0.0;
+    for (int64_t p = 0; p < n; ++p) {
+        if (ghat[p] > 0.0) L += g[p] * log(ghat[p]) - ghat[p];
+        else if (g[p] > 0.0) L += -INFINITY;
+    }
+    return L;
+}
+
+/* MLEM (Alg. 1) with the early stop Hagen recommends: iteration k evaluates
+ * L_k = L(f^(k)) on ghat = H f^(k) (Alg. 1 line 7), then updates f.  After update k >= 2 it stops
+ * when L_k - L_{k-1} <= rel_tol * |L_k| (reading R16), or after max_iters updates.
+ * ll[k-1] = L_k; returns the number of updates performed in *iters_done. */
+int oracle_mlem_monitored(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi,
+                          const int64_t* tap_ptr, const int64_t* tap_offset, const double* tap_weight,
+                          const double* g, double* f, int64_t max_iters, double rel_tol, double* ll,
+                          int64_t* iters_done) {
+    int rc = check_geom(a, alpha, w, gamma, xi);
+    if (rc) return rc;
+    int64_t n = gamma * xi, m = a * alpha * w;
+    double* h = (double*)malloc(sizeof(double) * (size_t)m);
+    double* gk = (double*)malloc(sizeof(double) * (size_t)n);
+    double* u = (double*)malloc(sizeof(double) * (size_t)n);
+    double* zeta = (double*)malloc(sizeof(double) * (size_t)m);
+    *iters_done = 0;
+    if (!h || !gk || !u || !zeta) { rc = OR_ENOMEM; goto done; }
+    if ((rc = oracle_sensitivity(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, h))) goto done;
+    for (int64_t k = 1; k <= max_iters; ++k) {
+        if ((rc = oracle_forward(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, f, gk))) goto done;
+        ll[k - 1] = oracle_loglik(n, g, gk);
+        for (int64_t p = 0; p < n; ++p) u[p] = gk[p] > 0.0 ? g[p] / gk[p] : 0.0;
+        if ((rc = oracle_backproject(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, u, zeta))) goto done;
+        for (int64_t j = 0; j < m; ++j) f[j] = (f[j] * zeta[j]) / h[j];
+        *iters_done = k;
+        if (k >= 2 && ll[k - 1] - ll[k - 2] <= rel_tol * fabs(ll[k - 1])) break;
+    }
+done:
+    free(h); free(gk); free(u); free(zeta);
+    return rc;
+}
+

@@ -311,3 +311,65 @@ def test_generator_shapes_and_determinism():
     s = syn.scene_blobs(syn.config("C2").geom)
     assert s.shape == (25, 64, 64) and s.dtype == np.float32 and abs(float(s.max()) - 100.0) < 1e-4
     assert np.array_equal(s, syn.scene_blobs(syn.config("C2").geom))
+
+
+# ------------------------------------------------------------------ §8(f) f-3: log-likelihood and early stop
+def test_loglik_matches_scipy_poisson_logpmf(oracle_lib):
+    """L = sum_p [g log ghat - ghat] is the Poisson log-likelihood up to the f-independent
+    -sum log(g_p!) (Shepp-Vardi): check against scipy.stats.poisson.logpmf on integer counts."""
+    from scipy.stats import poisson
+    from scipy.special import gammaln
+    cfg = syn.config("tiny")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    gbar = oracle_lib.forward(geom, taps, syn.scene_blobs(geom))
+    counts = syn.poisson_counts(gbar, seed=3, photons=2.0).astype(np.float64)
+    ghat = oracle_lib.forward(geom, taps, syn.scene_random(geom, seed=4, lo=0.5, hi=2.0)) * 2.0
+    want = float(np.sum(poisson.logpmf(counts, ghat)) + np.sum(gammaln(counts + 1.0)))
+    assert abs(oracle_lib.loglik(counts, ghat) - want) <= 1e-10 * abs(want)
+    # conventions (DESIGN.md R15): ghat = 0 with g = 0 contributes 0, with g > 0 gives -inf
+    assert oracle_lib.loglik([0.0, 1.0], [0.0, 1.0]) == -1.0
+    assert oracle_lib.loglik([1.0], [0.0]) == -np.inf
+
+
+def test_loglik_gradient_is_backprojection_minus_sensitivity(oracle_lib):
+    """dL/df_j = sum_p H_pj (g_p/ghat_p - 1) = (H^T (g/ghat))_j - h_j: central differences of the
+    oracle's L against its back projection and sensitivity (two independent code paths)."""
+    geom = syn.Geometry(5, 4, 2, 11, 9)
+    taps = syn.random_taps(geom, (2, 4), seed=8, region="any")
+    f = syn.scene_random(geom, seed=1, lo=0.5, hi=1.5).astype(np.float64).reshape(-1)
+    g = oracle_lib.forward(geom, taps, syn.scene_random(geom, seed=2, lo=0.5, hi=1.5))
+    ghat = oracle_lib.forward(geom, taps, f)
+    u = np.divide(g, ghat, out=np.zeros_like(g), where=ghat > 0)
+    grad = oracle_lib.backproject(geom, taps, u) - oracle_lib.sensitivity(geom, taps)
+    eps = 1e-6
+    for j in (0, 7, geom.m // 2, geom.m - 1):
+        fp, fm = f.copy(), f.copy()
+        fp[j] += eps
+        fm[j] -= eps
+        d = (oracle_lib.loglik(g, oracle_lib.forward(geom, taps, fp)) -
+             oracle_lib.loglik(g, oracle_lib.forward(geom, taps, fm))) / (2 * eps)
+        assert abs(d - grad[j]) <= 1e-6 * max(1.0, abs(grad[j]))
+
+
+def test_mlem_monitored_trace_and_early_stop(oracle_lib):
+    """Monitored MLEM: the log-likelihood rises every iteration (Shepp-Vardi); the iterate after
+    k updates is the plain MLEM iterate bit for bit; the stopping rule fires where it should."""
+    cfg = syn.config("tiny")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    g = syn.poisson_counts(oracle_lib.forward(geom, taps, syn.scene_blobs(geom)), seed=5, photons=1.0)
+    f, ll, k = oracle_lib.mlem_monitored(geom, taps, g, np.ones(geom.m), 40, -1.0)
+    assert k == 40 and np.all(np.diff(ll) > 0)
+    assert np.array_equal(f, oracle_lib.mlem(geom, taps, g, np.ones(geom.m), 40))
+    # L_k is the likelihood of f^(k): recompute it from the plain iterates
+    f3 = oracle_lib.mlem(geom, taps, g, np.ones(geom.m), 3)
+    assert ll[3] == oracle_lib.loglik(g, oracle_lib.forward(geom, taps, f3))
+    # huge tolerance: stops after the second update; tol 1e-4: first k with a small relative gain
+    assert oracle_lib.mlem_monitored(geom, taps, g, np.ones(geom.m), 40, 1e300)[2] == 2
+    _, _, k4 = oracle_lib.mlem_monitored(geom, taps, g, np.ones(geom.m), 40, 1e-4)
+    gains = (ll[1:] - ll[:-1]) / np.abs(ll[1:])
+    assert k4 == 2 + int(np.argmax(gains <= 1e-4))
+    # exact fixed point (g = H f, f0 = f): L is constant, the rule fires at k = 2 even with tol 0
+    ft = syn.scene_random(geom, seed=9, lo=0.5, hi=1.5).astype(np.float64).reshape(-1)
+    gf = oracle_lib.forward(geom, taps, ft)
+    _, llf, kf = oracle_lib.mlem_monitored(geom, taps, gf, ft, 10, 0.0)
+    assert kf == 2 and abs(llf[1] - llf[0]) <= 1e-12 * abs(llf[0])
