@@ -162,6 +162,22 @@ CTIS_API ctis_status ctis_back_update(ctis_plan plan, const float* r, float* f, 
 CTIS_API ctis_status ctis_back_update_from_ghat(ctis_plan plan, const float* g, const float* g_hat, float* f,
                                        void* ws, ctis_stream stream);
 
+/* MLEM with the per-iteration Poisson log-likelihood and an early stop (the paper
+ * recommends stopping early after Hagen; L is the objective EM ascends, shepp1982maximum):
+ *   iteration k (k = 1, 2, ...): g_hat = H f^(k); ll[k-1] = L_k = sum_p [g_p log g_hat_p - g_hat_p]
+ *   (pixels with g_hat_p <= 0 add 0 if g_p = 0, else -inf); r = g (/) g_hat; f^(k+1) = f (.) (H^T r) (/) h;
+ *   after update k >= 2 stop if L_k - L_{k-1} <= rel_tol * |L_k| (rel_tol <= 0: only an exact
+ *   stall stops), and always after max_iters updates.
+ * Single frame.  g[n] read only, f[m] in place (f^(1) in, f^(iters_done+1) out), ws as ctis_mlem.
+ * ll: DEVICE array of max_iters doubles (8-byte aligned; entries >= iters_done are 0);
+ * iters_done: DEVICE int (4-byte aligned), the number of updates performed.  The loop runs on the
+ * device (a CUDA-graph conditional WHILE node): no host round trip per iteration.  L is accumulated
+ * in fp64 from fp32 g_hat (logf).  Errors: as ctis_mlem; CTIS_ERR_UNSUPPORTED if the driver lacks
+ * conditional graph nodes; max_iters < 0 -> CTIS_ERR_INVALID_ARGUMENT; max_iters = 0 sets
+ * *iters_done = 0 and leaves f unchanged. */
+CTIS_API ctis_status ctis_mlem_monitored(ctis_plan plan, const float* g, float* f, int max_iters, double rel_tol,
+                                         void* ws, double* ll, int* iters_done, ctis_stream stream);
+
 /* End-to-end convenience on HOST buffers: copies g_host[frames][n] and
  * f_host[frames][m] (f0) to plan-owned device buffers, runs ctis_mlem_batched,
  * copies f back into f_host and synchronises `stream` before returning.

@@ -42,6 +42,7 @@ _SIGS = {
     "ctis_sensitivity": ([_P, _P, _P], _int),
     "ctis_mlem": ([_P, _P, _P, _int, _P, _P], _int),
     "ctis_mlem_batched": ([_P, _P, _P, _i64, _int, _P, _P], _int),
+    "ctis_mlem_monitored": ([_P, _P, _P, _int, ctypes.c_double, _P, _P, _P, _P], _int),
     "ctis_back_update_from_ghat": ([_P, _P, _P, _P, _P, _P], _int),
     "ctis_forward_ratio": ([_P, _P, _P, _P, _P], _int),
     "ctis_back_update": ([_P, _P, _P, _P], _int),
@@ -212,6 +213,21 @@ class Plan:
             _check(_lib.ctis_mlem_batched(self._h, gp, fp, frames, int(iters), ctypes.c_void_p(ws.data_ptr()),
                                           _stream_handle(stream)), "ctis_mlem_batched")
         return f
+
+    def mlem_monitored(self, g, f, max_iters: int, rel_tol: float = 0.0, ws=None, stream=None):
+        """In-place MLEM with the per-iteration Poisson log-likelihood and the early stop
+        (ctis_mlem_monitored; R15/R16).  Returns (ll, iters_done) as device tensors:
+        ll float64[max_iters] (L_k of f^(k); zero past iters_done), iters_done int32[1]."""
+        import torch
+        ws = self.workspace(1) if ws is None else ws
+        dev = f.device
+        ll = torch.empty(max(int(max_iters), 1), dtype=torch.float64, device=dev)
+        done = torch.empty(1, dtype=torch.int32, device=dev)
+        _check(_lib.ctis_mlem_monitored(self._h, _dev_ptr(g, self.n, "g"), _dev_ptr(f, self.m, "f"), int(max_iters),
+                                        float(rel_tol), ctypes.c_void_p(ws.data_ptr()),
+                                        ctypes.c_void_p(ll.data_ptr()), ctypes.c_void_p(done.data_ptr()),
+                                        _stream_handle(stream)), "ctis_mlem_monitored")
+        return ll, done
 
     def forward_ratio(self, f, g, r, stream=None):
         """r = g (/) (H f) (Alg. 1 lines 6-8, one fused kernel)."""

@@ -67,6 +67,20 @@ struct GraphKey {
   }
 };
 
+// Monitored MLEM graphs (conditional WHILE node) are keyed by every buffer and parameter they bake in.
+struct MonKey {
+  const void* g;
+  void* f;
+  void* ws;
+  void* ll;
+  void* cnt;
+  int max_iters;
+  double tol;
+  bool operator<(const MonKey& o) const {
+    return std::tie(g, f, ws, ll, cnt, max_iters, tol) < std::tie(o.g, o.f, o.ws, o.ll, o.cnt, o.max_iters, o.tol);
+  }
+};
+
 // One 64 KB __constant__ page of tap tables and the library instance that owns it.
 struct Page {
   bool forward = true;
@@ -105,12 +119,14 @@ struct ctis_plan_s {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<MonKey, cudaGraphExec_t> mon_graphs;
   int64_t last_launches = 0;
   std::mutex mu;
 
   ~ctis_plan_s() {
     DeviceGuard dg(device);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : mon_graphs) cudaGraphExecDestroy(kv.second);
     if (side) cudaStreamDestroy(side);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
@@ -982,6 +998,107 @@ ctis_status run_mlem(ctis_plan_s& P, const float* g, float* f, int64_t frames, i
   return CTIS_OK;
 }
 
+// Monitored MLEM (ctis_mlem_monitored): [memset g_hat, ll, counter] -> WHILE { forward; ratio + L;
+// back + update; stop rule } as one instantiated graph; the WHILE body runs until the device-side
+// check clears the condition.
+ctis_status run_mlem_monitored(ctis_plan_s& P, const float* g, float* f, int max_iters, double rel_tol, void* ws,
+                               double* ll, int* cnt, cudaStream_t s) {
+  if (P.shard)
+    return fail(CTIS_ERR_INVALID_ARGUMENT, "mlem on a shard plan needs the collective (see ctis_back_update_from_ghat)");
+  if (max_iters < 0) return fail(CTIS_ERR_INVALID_ARGUMENT, "max_iters < 0");
+  ctis_status st = check_ptrs({g, f, ws});
+  if (st) return st;
+  if (!ll || !cnt || (reinterpret_cast<uintptr_t>(ll) & 7u) || (reinterpret_cast<uintptr_t>(cnt) & 3u))
+    return fail(CTIS_ERR_INVALID_ARGUMENT, "ll (8-byte aligned) and iters_done (4-byte aligned) must be device pointers");
+  DeviceGuard dg(P.device);
+  P.last_launches = 0;
+  if (P.validate) {
+    if ((st = validate_data(P, g, f, 1, s))) return st;
+    P.last_launches += 2;
+  }
+  if (max_iters == 0) {
+    CTIS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int), s), "iters_done");
+    return CTIS_OK;
+  }
+  float* A = static_cast<float*>(ws);
+  float* B = A + (((size_t)P.n + 3) & ~(size_t)3);
+  MonKey key{g, f, ws, ll, cnt, max_iters, rel_tol};
+  auto it = P.mon_graphs.find(key);
+  int64_t body_launches = 0;
+  if (it == P.mon_graphs.end()) {
+    if (P.mon_graphs.size() >= 16) {
+      for (auto& kv : P.mon_graphs) cudaGraphExecDestroy(kv.second);
+      P.mon_graphs.clear();
+    }
+    cudaGraph_t graph = nullptr;
+    CTIS_CUDA(cudaGraphCreate(&graph, 0), "graph create");
+    auto bail = [&](cudaError_t e, const char* where) {
+      cudaGraphDestroy(graph);
+      return e == cudaErrorNotSupported || e == cudaErrorInvalidValue
+                 ? fail(CTIS_ERR_UNSUPPORTED, std::string(where) + ": " + cudaGetErrorString(e))
+                 : cuda_fail(e, where);
+    };
+    cudaGraphNode_t prev = nullptr, node = nullptr;
+    auto memset_node = [&](void* ptr, size_t words) -> cudaError_t {
+      cudaMemsetParams mp{};
+      mp.dst = ptr;
+      mp.value = 0;
+      mp.elementSize = 4;
+      mp.width = words;
+      mp.height = 1;
+      mp.pitch = 0;
+      cudaError_t e = cudaGraphAddMemsetNode(&node, graph, prev ? &prev : nullptr, prev ? 1 : 0, &mp);
+      prev = node;
+      return e;
+    };
+    cudaError_t e = memset_node(A, (size_t)P.n);
+    if (e == cudaSuccess) e = memset_node(ll, 2 * (size_t)max_iters);
+    if (e == cudaSuccess) e = memset_node(cnt, 1);
+    if (e != cudaSuccess) return bail(e, "memset nodes");
+    cudaGraphConditionalHandle handle;
+    e = cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault);
+    if (e != cudaSuccess) return bail(e, "cudaGraphConditionalHandleCreate");
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    e = cudaGraphAddNode(&node, graph, &prev, 1, &cp);
+    if (e != cudaSuccess) return bail(e, "conditional WHILE node");
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(P.side, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return bail(e, "capture to WHILE body");
+    cudaError_t e1 = enqueue_forward(P, f, A, 1, P.side, &body_launches);
+    if (e1 == cudaSuccess) {
+      e1 = launch_ratio_ll(g, A, B, P.n, ll, cnt, P.side);
+      ++body_launches;
+    }
+    if (e1 == cudaSuccess) e1 = enqueue_back(P, B, f, 1, 1, P.side, &body_launches);
+    if (e1 == cudaSuccess) {
+      e1 = launch_mlem_check(ll, cnt, max_iters, rel_tol, (unsigned long long)handle, P.side);
+      ++body_launches;
+    }
+    cudaGraph_t captured = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(P.side, &captured);
+    if (e1 != cudaSuccess) return bail(e1, "WHILE body launches");
+    if (e2 != cudaSuccess) return bail(e2, "end capture (WHILE body)");
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e, "graph instantiate (monitored MLEM)");
+    it = P.mon_graphs.emplace(key, exec).first;
+  } else {
+    body_launches = (int64_t)P.fwd.size() + (int64_t)P.back.size() + 2;
+  }
+  CTIS_CUDA(cudaEventRecord(P.ev_in, s), "event record");
+  CTIS_CUDA(cudaStreamWaitEvent(P.side, P.ev_in, 0), "stream wait");
+  CTIS_CUDA(cudaGraphLaunch(it->second, P.side), "graph launch");
+  CTIS_CUDA(cudaEventRecord(P.ev_out, P.side), "event record");
+  CTIS_CUDA(cudaStreamWaitEvent(s, P.ev_out, 0), "stream wait");
+  P.last_launches += body_launches;  // per iteration of the device-side loop
+  return CTIS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1110,6 +1227,13 @@ ctis_status ctis_mlem_batched(ctis_plan p, const float* g, float* f, int64_t fra
   if (!p) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL plan");
   std::lock_guard<std::mutex> lk(p->mu);
   return run_mlem(*p, g, f, frames, iters, ws, (cudaStream_t)stream);
+}
+
+ctis_status ctis_mlem_monitored(ctis_plan p, const float* g, float* f, int max_iters, double rel_tol, void* ws,
+                                double* ll, int* iters_done, ctis_stream stream) {
+  if (!p) return fail(CTIS_ERR_INVALID_ARGUMENT, "plan is NULL");
+  std::lock_guard<std::mutex> lk(p->mu);
+  return run_mlem_monitored(*p, g, f, max_iters, rel_tol, ws, ll, iters_done, (cudaStream_t)stream);
 }
 
 ctis_status ctis_back_update_from_ghat(ctis_plan p, const float* g, const float* g_hat, float* f, void* ws,

@@ -72,4 +72,59 @@ cudaError_t launch_validate(const float* x, long long count, int* flag, cudaStre
   return cudaGetLastError();
 }
 
+// Ratio + Poisson log-likelihood of the current model (R15): each thread accumulates its
+// terms in fp64, the block reduces them (warp shuffles, then shared memory) and adds one value to
+// ll[*counter] with a double-precision atomic.
+__global__ void ratio_ll_kernel(const float* __restrict__ g, float* gh, float* r, long long count, double* ll,
+                                const int* __restrict__ counter) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += stride) {
+    const float gv = __ldg(g + i), hv = gh[i];
+    r[i] = hv > 0.f ? __fdiv_rn(gv, hv) : 0.f;
+    gh[i] = 0.f;
+    if (hv > 0.f)
+      acc += (double)gv * (double)logf(hv) - (double)hv;
+    else if (gv > 0.f)
+      acc = -INFINITY;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double part[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) part[warp] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    double v = lane < (int)(blockDim.x >> 5) ? part[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) atomicAdd(ll + *counter, v);
+  }
+}
+
+cudaError_t launch_ratio_ll(const float* g, float* ghat, float* r, long long count, double* ll, const int* counter,
+                            cudaStream_t s) {
+  const long long want = (count + 255) / 256;
+  const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
+  ratio_ll_kernel<<<blocks, 256, 0, s>>>(g, ghat, r, count, ll, counter);
+  return cudaGetLastError();
+}
+
+// Stop rule after update k = *counter + 1 (R16), evaluated on the device: sets the WHILE
+// node's condition so the graph itself decides whether the next iteration runs.
+__global__ void mlem_check_kernel(const double* __restrict__ ll, int* counter, int max_iters, double rel_tol,
+                                  cudaGraphConditionalHandle handle) {
+  const int k = *counter + 1;
+  *counter = k;
+  bool stop = k >= max_iters;
+  if (k >= 2 && ll[k - 1] - ll[k - 2] <= rel_tol * fabs(ll[k - 1])) stop = true;
+  cudaGraphSetConditional(handle, stop ? 0u : 1u);
+}
+
+cudaError_t launch_mlem_check(const double* ll, int* counter, int max_iters, double rel_tol,
+                              unsigned long long cond_handle, cudaStream_t s) {
+  mlem_check_kernel<<<1, 1, 0, s>>>(ll, counter, max_iters, rel_tol, (cudaGraphConditionalHandle)cond_handle);
+  return cudaGetLastError();
+}
+
 }  // namespace ctis

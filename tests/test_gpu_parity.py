@@ -295,3 +295,55 @@ def test_no_stale_shared_memory_reads(ctis):
     r = subprocess.run([sys.executable, os.path.join(here, "poison_case.py")], env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------ §8(f) f-3: log-likelihood, early stop, H^T g init
+@pytest.mark.parametrize("name,photons,tol", [("tiny", 1.0, 1e-4), ("C2", 4.0, 1e-5), ("C3", 2.0, 3e-6)])
+def test_mlem_monitored_vs_oracle(ctis, oracle_lib, dev, name, photons, tol):
+    """Poisson-count frames: the device-side loop's log-likelihood trace matches the oracle's, the
+    GPU stops exactly where its own trace satisfies the rule (R16, decided in the kernel's
+    fp64), and f equals the oracle's plain MLEM iterate after that many updates."""
+    cfg = syn.config(name)
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    g = syn.poisson_counts(oracle_lib.forward(geom, taps, syn.scene_blobs(geom)), seed=11, photons=photons)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    fd = torch.ones(geom.m, dtype=torch.float32, device=dev)
+    ll, done = plan.mlem_monitored(cuda(g, dev), fd, cfg.K, tol)
+    k = int(done.item())
+    ll = ll.cpu().numpy()
+    assert 2 <= k <= cfg.K and np.all(ll[k:] == 0.0)
+    _, ll_o, k_o = oracle_lib.mlem_monitored(geom, taps, g, np.ones(geom.m), cfg.K, -1.0)
+    assert np.all(np.abs(ll[:k] - ll_o[:k]) <= 1e-5 * np.abs(ll_o[:k]))
+    gains = (ll[1:k] - ll[:k - 1]) <= tol * np.abs(ll[1:k])
+    want_k = 2 + int(np.argmax(gains)) if gains.any() else cfg.K
+    assert k == want_k
+    assert rel(fd.cpu().numpy(), oracle_lib.mlem(geom, taps, g, np.ones(geom.m), k)) <= MLEM_TOL
+
+
+def test_mlem_monitored_runs_all_iterations_and_zero(ctis, oracle_lib, dev):
+    cfg = syn.config("tiny")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    g = oracle_lib.forward(geom, taps, syn.scene_blobs(geom)).astype(np.float32)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    fd = torch.ones(geom.m, dtype=torch.float32, device=dev)
+    ll, done = plan.mlem_monitored(cuda(g, dev), fd, 25, -1.0)
+    assert int(done.item()) == 25 and np.all(np.diff(ll.cpu().numpy()) > 0)
+    f2 = torch.ones(geom.m, dtype=torch.float32, device=dev)
+    plan.mlem(cuda(g, dev), f2, 25)
+    assert rel(fd.cpu().numpy(), f2.cpu().numpy()) <= 1e-6  # same kernels as ctis_mlem (atomic order aside)
+    f3 = torch.ones(geom.m, dtype=torch.float32, device=dev)
+    _, done0 = plan.mlem_monitored(cuda(g, dev), f3, 0, 1e-3)
+    assert int(done0.item()) == 0 and bool((f3 == 1).all())
+
+
+def test_mlem_from_backprojection_init(ctis, oracle_lib, dev):
+    """f^(1) = H^T g, the paper's other initial guess: ctis_backproject then ctis_mlem."""
+    cfg = syn.config("C2")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    g = oracle_lib.forward(geom, taps, syn.scene_blobs(geom)).astype(np.float32)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    f0 = plan.backproject(cuda(g, dev))
+    assert rel(f0.cpu().numpy(), oracle_lib.backproject(geom, taps, g)) <= PROJ_TOL
+    plan.mlem(cuda(g, dev), f0, 30)
+    want = oracle_lib.mlem(geom, taps, g, oracle_lib.backproject(geom, taps, g), 30)
+    assert rel(f0.cpu().numpy(), want) <= MLEM_TOL
