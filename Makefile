@@ -4,7 +4,7 @@ PKG      := paper_2006_01573_b200
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden \
             --expt-relaxed-constexpr -Iinclude -Ibuild
-HDRS     := include/ctis.h $(PKG)/csrc/ctis_internal.h $(PKG)/csrc/ctis_kernels.h
+HDRS     := include/ctis.h $(PKG)/csrc/ctis_internal.h $(PKG)/csrc/ctis_kernels.h $(PKG)/csrc/ctis_fft.h
 
 all: $(PKG)/libctis.so oracle/liboracle.so
 
@@ -23,12 +23,16 @@ build/ctis_api.o: $(PKG)/csrc/ctis_api.cu $(HDRS)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
+build/ctis_fft.o: $(PKG)/csrc/ctis_fft.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
 build/ctis_kernels.o: $(PKG)/csrc/ctis_kernels.cu $(HDRS)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> build/ctis_kernels.ptxas.log || (cat build/ctis_kernels.ptxas.log; false)
 
-$(PKG)/libctis.so: build/ctis_api.o build/ctis_kernels.o build/ctis_tables_blob.o
-	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC -o $@.tmp $^ && mv $@.tmp $@
+$(PKG)/libctis.so: build/ctis_api.o build/ctis_kernels.o build/ctis_fft.o build/ctis_tables_blob.o
+	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC -o $@.tmp $^ -lcufft && mv $@.tmp $@
 
 oracle/liboracle.so: oracle/ctis_oracle.c
 	gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -std=c99 -o $@ $<

@@ -76,8 +76,14 @@ typedef enum {
   CTIS_OPT_VALIDATE_DATA = 1,   /* 1 (default): ctis_mlem* check g >= 0, f0 >= 0, finite, with one
                                    reduction kernel and ONE host synchronisation per call;
                                    0: skip (the call is then fully asynchronous). */
-  CTIS_OPT_USE_GRAPH = 2        /* 1 (default): ctis_mlem* replay a captured CUDA graph of the
+  CTIS_OPT_USE_GRAPH = 2,       /* 1 (default): ctis_mlem* replay a captured CUDA graph of the
                                    iterations; 0: launch kernels directly on `stream`. */
+  CTIS_OPT_PROJECTOR = 3        /* 0 (default): the tap projector.  1: the paper's own Fourier route
+                                   (Eqs. 13 and 17 with cuFFT, d_i = F c_i precomputed; Alg. 1
+                                   lines 6-11) for every ctis_forward / _backproject / _mlem* call on the
+                                   plan — a comparator arm.  Allocates O(w n) complex
+                                   scratch owned by the plan (CTIS_ERR_OUT_OF_MEMORY if it does not fit):
+                                   calls on one plan must then not run concurrently on different streams. */
 } ctis_option;
 
 /* Create a plan for the full operator H (all w bands).

@@ -61,7 +61,7 @@ EXPORTED = tuple(_SIGS)
 # status codes (include/ctis.h)
 OK, ERR_INVALID_ARGUMENT, ERR_DIMENSION, ERR_TAP, ERR_ZERO_SENSITIVITY, ERR_DATA, ERR_CUDA, \
     ERR_OUT_OF_MEMORY, ERR_UNSUPPORTED = range(9)
-OPT_VALIDATE_DATA, OPT_USE_GRAPH = 1, 2
+OPT_VALIDATE_DATA, OPT_USE_GRAPH, OPT_PROJECTOR = 1, 2, 3
 
 
 class CtisError(RuntimeError):

@@ -17,6 +17,7 @@
 
 #include "../../include/ctis.h"
 #include "ctis_internal.h"
+#include "ctis_fft.h"
 #include "ctis_kernels.h"
 // the projection-kernel cubin, embedded by build/ctis_tables_blob.S (.incbin)
 extern "C" const unsigned char ctis_tables_cubin[], ctis_tables_cubin_end[];
@@ -120,6 +121,10 @@ struct ctis_plan_s {
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<MonKey, cudaGraphExec_t> mon_graphs;
+  int projector = 0;                 // CTIS_OPT_PROJECTOR: 0 taps (default), 1 the paper's FFT route
+  ctis::FftState* fft = nullptr;     // created when the FFT projector is selected
+  std::vector<std::vector<std::pair<int64_t, float>>> band_taps;  // (offset, weight) per local band
+  std::vector<float> inv_h;          // 1 / h_lambda per local band
   int64_t last_launches = 0;
   std::mutex mu;
 
@@ -127,6 +132,7 @@ struct ctis_plan_s {
     DeviceGuard dg(device);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : mon_graphs) cudaGraphExecDestroy(kv.second);
+    ctis::fft_destroy(fft);
     if (side) cudaStreamDestroy(side);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
@@ -763,10 +769,12 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
     }
     std::sort(bt.begin(), bt.end());
     for (auto& x : bt) bands[lam].push_back(TapXY{(int)(x.first % gamma), (int)(x.first / gamma), x.second});
+    p->band_taps.push_back(bt);
     invh[lam] = (float)(1.0 / hs);
     hloc[lam] = hband[l];
     p->total_taps += (int64_t)bt.size();
   }
+  p->inv_h = invh;
   ctis_status st = build_tables(*p, bands, invh);
   cudaError_t e = cudaSuccess;
   if (!st) {
@@ -906,11 +914,25 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
 
 // g_hat (accumulated with red.add: must be zero on entry) += H f
 cudaError_t enqueue_forward(ctis_plan_s& P, const float* f, float* ghat, int frames, cudaStream_t s, int64_t* cnt) {
+  if (P.projector == 1) {  // the paper's Fourier route (comparator arm)
+    for (int z = 0; z < frames; ++z) {
+      cudaError_t e = fft_forward_accumulate(P.fft, f + (size_t)z * P.m, ghat + (size_t)z * P.n, s, cnt);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   return launch_pages(P, P.fwd, f, ghat, P.m, P.n, frames, 0, s, cnt);
 }
 
 cudaError_t enqueue_back(ctis_plan_s& P, const float* r, float* fz, int frames, int mode, cudaStream_t s,
                          int64_t* cnt) {
+  if (P.projector == 1) {
+    for (int z = 0; z < frames; ++z) {
+      cudaError_t e = fft_back(P.fft, r + (size_t)z * P.n, fz + (size_t)z * P.m, mode, s, cnt);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   return launch_pages(P, P.back, r, fz, P.n, P.m, frames, mode, s, cnt);
 }
 
@@ -1129,6 +1151,25 @@ ctis_status ctis_set_option(ctis_plan p, int option, int64_t value) {
   switch (option) {
     case CTIS_OPT_VALIDATE_DATA: p->validate = value != 0; return CTIS_OK;
     case CTIS_OPT_USE_GRAPH: p->use_graph = value != 0; return CTIS_OK;
+    case CTIS_OPT_PROJECTOR: {
+      if (value != 0 && value != 1) return fail(CTIS_ERR_INVALID_ARGUMENT, "projector must be 0 (taps) or 1 (FFT)");
+      if (value == 1 && !p->fft) {
+        if ((long long)p->w * ((long long)p->n / 2 + 1) >= (1LL << 31))
+          return fail(CTIS_ERR_UNSUPPORTED, "FFT projector: w * (n/2 + 1) must be < 2^31");
+        DeviceGuard dg(p->device);
+        cudaError_t e = fft_create(&p->fft, p->a, p->alpha, p->w, p->gamma, p->xi, p->band_taps, p->inv_h);
+        if (e == cudaErrorMemoryAllocation) return fail(CTIS_ERR_OUT_OF_MEMORY, "FFT projector buffers");
+        if (e != cudaSuccess) return cuda_fail(e, "FFT projector setup (cuFFT)");
+      }
+      if (p->projector != (int)value) {  // captured graphs bake the projector in
+        for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+        p->graphs.clear();
+        for (auto& kv : p->mon_graphs) cudaGraphExecDestroy(kv.second);
+        p->mon_graphs.clear();
+      }
+      p->projector = (int)value;
+      return CTIS_OK;
+    }
     default: return fail(CTIS_ERR_INVALID_ARGUMENT, "unknown option");
   }
 }

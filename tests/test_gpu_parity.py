@@ -347,3 +347,39 @@ def test_mlem_from_backprojection_init(ctis, oracle_lib, dev):
     plan.mlem(cuda(g, dev), f0, 30)
     want = oracle_lib.mlem(geom, taps, g, oracle_lib.backproject(geom, taps, g), 30)
     assert rel(f0.cpu().numpy(), want) <= MLEM_TOL
+
+
+# ------------------------------------------------------------------ §8(f) f-2: the paper's FFT projector (comparator)
+@pytest.mark.parametrize("name", ["tiny", "C2"])
+def test_fft_projector_vs_oracle(ctis, oracle_lib, dev, name):
+    """CTIS_OPT_PROJECTOR = 1 (Eqs. 13/17 with cuFFT) computes the same H as the taps (fp32 FFT
+    round-off: relative L2 <= 1e-5 per projection, <= 1e-3 on f after K iterations)."""
+    cfg = syn.config(name)
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    plan.set_option(ctis.OPT_PROJECTOR, 1)
+    f = syn.scene_blobs(geom)
+    g = oracle_lib.forward(geom, taps, f)
+    assert rel(plan.forward(cuda(f, dev)).cpu().numpy(), g) <= PROJ_TOL
+    u = np.random.default_rng(1).uniform(0.5, 1.5, geom.n).astype(np.float32)
+    assert rel(plan.backproject(cuda(u, dev)).cpu().numpy(), oracle_lib.backproject(geom, taps, u)) <= PROJ_TOL
+    g32 = g.astype(np.float32)
+    fd = torch.ones(geom.m, dtype=torch.float32, device=dev)
+    plan.mlem(cuda(g32, dev), fd, cfg.K)
+    assert rel(fd.cpu().numpy(), oracle_lib.mlem(geom, taps, g32, np.ones(geom.m), cfg.K)) <= MLEM_TOL
+
+
+def test_fft_projector_wrapping_taps_and_switch_back(ctis, oracle_lib, dev):
+    """The Fourier route is the 1-D circulant of Eq. 7, wrap included; switching back to the taps
+    (option 0) restores the tap kernels (graphs are re-captured)."""
+    geom = syn.Geometry(33, 17, 6, 70, 45)
+    taps = syn.random_taps(geom, (2, 9), seed=77, region="any")
+    plan = ctis.Plan.from_geometry(geom, taps)
+    f = syn.scene_random(geom, seed=3, lo=0.1, zero_frac=0.1)
+    g = oracle_lib.forward(geom, taps, f).astype(np.float32)
+    for proj in (1, 0, 1):
+        plan.set_option(ctis.OPT_PROJECTOR, proj)
+        assert rel(plan.forward(cuda(f, dev)).cpu().numpy(), oracle_lib.forward(geom, taps, f)) <= PROJ_TOL
+        fd = torch.ones(geom.m, dtype=torch.float32, device=dev)
+        plan.mlem(cuda(g, dev), fd, 10)
+        assert rel(fd.cpu().numpy(), oracle_lib.mlem(geom, taps, g, np.ones(geom.m), 10)) <= MLEM_TOL
