@@ -491,13 +491,13 @@ std::vector<std::pair<int, int>> balanced_chunks(int w, int maxb) {
 int choose_back_nb(const ctis_plan_s& P) {
   if (const char* e = std::getenv("CTIS_BACK_NB")) {  // experiments: 4, 8, 12 or 16
     const int v = std::atoi(e);
-    if (v == 4 || v == 8 || v == 12 || v == 16) return v;
+    if (v == 2 || v == 4 || v == 8 || v == 12 || v == 16) return v;
   }
   const long long tiles = (long long)((P.a + kBackTR - 1) / kBackTR) * ((P.alpha + kBackTC - 1) / kBackTC);
   const long long slots = 148LL * 2;
   int best = kBackBandsMax;
   double bestc = 1e300;
-  for (int NB : {16, 12, 8, 4}) {
+  for (int NB : {16, 12, 8, 4, 2}) {
     const long long nch = (P.w + NB - 1) / NB;
     const long long ctas = tiles * nch;
     const double waves = std::ceil((double)ctas / (double)slots);
@@ -525,6 +525,14 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     if (P.tma_f) {
       fbands = kFwdBandsTma;  // measured at C4: 16/12 -> 85.3 us, 25/16 -> 82.2 us (C3: 23.0 -> 19.0 us)
       fspan = kModeSpanTma;
+      // small problems: shorter chunks until the persistent grid (2 CTAs per SM) has enough work
+      // items (tiles x mode passes x chunks) to keep every SM busy
+      size_t tmax = 1;
+      for (const auto& b : bands) tmax = std::max(tmax, b.size());
+      const long long tiles = (long long)((P.a + 2 * fspan + kFwdTR - 1) / kFwdTR) *
+                              ((P.alpha + 2 * fspan + kFwdTC - 1) / kFwdTC);
+      const long long passes = ((long long)tmax + 31) / 32;
+      while (fbands > 1 && tiles * passes * ((P.w + fbands - 1) / fbands) < 2LL * P.sms) fbands = fbands / 2;
       if (const char* e = std::getenv("CTIS_FWD_BANDS")) fbands = std::max(1, std::atoi(e));
       if (const char* e = std::getenv("CTIS_FWD_SPAN")) fspan = std::max(1, std::min(kModeSpanMax, std::atoi(e)));
     }

@@ -41,7 +41,7 @@ constexpr int kFwdTC = 16;
 constexpr int kFwdThreads = kFwdTR * kFwdTC;   // per group
 constexpr int kFwd2Threads = kFwdThreads / 2;  // two u positions per thread (forward_persistent2)
 constexpr int kFwdBands = 16;           // default max bands per forward chunk (chunks are balanced)
-// Back kernel geometry: 32 x 32 voxel tile, 2 voxels per thread, NB in {4, 8, 12, 16} bands
+// Back kernel geometry: 32 x 32 voxel tile, 2 voxels per thread, NB in {2, 4, 8, 12, 16} bands
 // per chunk (kernel template; the plan picks the one that fills the 148 SMs best).
 constexpr int kBackTR = 32;
 constexpr int kBackTC = 32;

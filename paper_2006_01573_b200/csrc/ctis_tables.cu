@@ -1131,6 +1131,7 @@ CTIS_FWD2(4, 4, 16)
     if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                             \
     back_persistent4<NB>(A, &tm);                                                                          \
   }
+CTIS_BACK4(2)
 CTIS_BACK4(4)
 CTIS_BACK4(8)
 CTIS_BACK4(12)
@@ -1149,6 +1150,7 @@ CTIS_BACK4(16)
     if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                                 \
     back_body<NB, false, true>(A, &tm);                                                                    \
   }
+CTIS_BACK(2)
 CTIS_BACK(4)
 CTIS_BACK(8)
 CTIS_BACK(12)
