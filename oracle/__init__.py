@@ -62,6 +62,8 @@ def _load():
             lib.oracle_loglik.restype = ctypes.c_double
             lib.oracle_mlem_monitored.argtypes = geo + [P, P, P, P, P, i64, ctypes.c_double, P, P]
             lib.oracle_mlem_monitored.restype = ctypes.c_int
+            lib.oracle_smart.argtypes = geo + [P, P, P, P, P, i64]
+            lib.oracle_smart.restype = ctypes.c_int
             lib.oracle_mlem.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -164,4 +166,15 @@ def mlem_monitored(geom, taps, g, f0, max_iters: int, rel_tol: float):
                                      int(max_iters), float(rel_tol), _ptr(ll), _ptr(done)), "mlem_monitored")
     k = int(done[0])
     return f, ll[:k], k
+
+
+def smart(geom, taps, g, f0, iters: int) -> np.ndarray:
+    """SMART (simultaneous MART) in float64 (oracle_smart): returns f after `iters` updates."""
+    lib = _load()
+    ptr, off, wt = _taps(taps)
+    gd = np.ascontiguousarray(np.asarray(g, np.float64).reshape(-1))
+    f = np.array(np.asarray(f0, np.float64).reshape(-1), copy=True)
+    assert gd.size == geom.n and f.size == geom.m
+    _check(lib.oracle_smart(*_geo(geom), _ptr(ptr), _ptr(off), _ptr(wt), _ptr(gd), _ptr(f), int(iters)), "smart")
+    return f
 

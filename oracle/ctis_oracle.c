@@ -233,3 +233,31 @@ done:
     return rc;
 }
 
+/* SMART, the simultaneous (data-parallel) form of the MART solver the paper lists (
+ * gordon1970algebraic), on the same projector:
+ *   f_j <- f_j * exp( (1/h_j) sum_i H_ij log(g_i / (H f)_i) )
+ * with log-ratio r_i = log(g_i / ghat_i) where g_i > 0 and ghat_i > 0, else 0 (R17).
+ * Step order as Alg. 1 with the ratio replaced by the log-ratio and the update by the exponential. */
+int oracle_smart(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi,
+                 const int64_t* tap_ptr, const int64_t* tap_offset, const double* tap_weight,
+                 const double* g, double* f, int64_t iters) {
+    int rc = check_geom(a, alpha, w, gamma, xi);
+    if (rc) return rc;
+    int64_t n = gamma * xi, m = a * alpha * w;
+    double* h = (double*)malloc(sizeof(double) * (size_t)m);
+    double* gk = (double*)malloc(sizeof(double) * (size_t)n);
+    double* u = (double*)malloc(sizeof(double) * (size_t)n);
+    double* zeta = (double*)malloc(sizeof(double) * (size_t)m);
+    if (!h || !gk || !u || !zeta) { rc = OR_ENOMEM; goto done; }
+    if ((rc = oracle_sensitivity(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, h))) goto done;
+    for (int64_t k = 0; k < iters; ++k) {
+        if ((rc = oracle_forward(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, f, gk))) goto done;
+        for (int64_t p = 0; p < n; ++p) u[p] = (g[p] > 0.0 && gk[p] > 0.0) ? log(g[p] / gk[p]) : 0.0;
+        if ((rc = oracle_backproject(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, u, zeta))) goto done;
+        for (int64_t j = 0; j < m; ++j) f[j] = f[j] * exp(zeta[j] / h[j]);
+    }
+done:
+    free(h); free(gk); free(u); free(zeta);
+    return rc;
+}
+

@@ -373,3 +373,51 @@ def test_mlem_monitored_trace_and_early_stop(oracle_lib):
     gf = oracle_lib.forward(geom, taps, ft)
     _, llf, kf = oracle_lib.mlem_monitored(geom, taps, gf, ft, 10, 0.0)
     assert kf == 2 and abs(llf[1] - llf[0]) <= 1e-12 * abs(llf[0])
+
+
+# ------------------------------------------------------------------ §8(f) f-4: SMART (simultaneous MART)
+def _kl(a, b):
+    """Kullback-Leibler distance KL(a, b) = sum a log(a/b) + b - a (0 log 0 = 0)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    t = np.where(a > 0, a * np.log(np.where(a > 0, a, 1.0) / np.where(b > 0, b, 1.0)), 0.0)
+    return float(np.sum(t + b - a))
+
+
+def test_smart_decreases_kl_and_fixed_point(oracle_lib):
+    """SMART minimises KL(Hf, g) and decreases it at every step for consistent positive data
+    (Byrne 1993); a fixed point Hf = g is left unchanged; one step equals the dense-H update."""
+    cfg = syn.config("tiny")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    ft = syn.scene_random(geom, seed=5, lo=0.5, hi=1.5)
+    g = oracle_lib.forward(geom, taps, ft)
+    f = np.ones(geom.m)
+    kl = []
+    for k in range(30):
+        kl.append(_kl(oracle_lib.forward(geom, taps, f), g))
+        f = oracle_lib.smart(geom, taps, g, f, 1)
+    assert np.all(np.diff(kl) < 0)
+    assert np.array_equal(oracle_lib.smart(geom, taps, g, np.ones(geom.m), 30), f)
+    fx = oracle_lib.smart(geom, taps, g, ft, 3)
+    assert np.max(np.abs(fx - ft.reshape(-1))) <= 1e-12 * np.max(ft)
+    # dense H (Eqs. 3-7): f <- f * exp(H^T log(g / Hf) / h)
+    geom2 = syn.Geometry(4, 3, 2, 9, 7)
+    taps2 = syn.random_taps(geom2, (2, 4), seed=2, region="any")
+    H = dense.dense_H(geom2, taps2)
+    f0 = syn.scene_random(geom2, seed=1, lo=0.5, hi=1.5).astype(np.float64).reshape(-1)
+    g2 = H @ syn.scene_random(geom2, seed=2, lo=0.5, hi=1.5).astype(np.float64).reshape(-1)
+    gh = H @ f0
+    u = np.where((g2 > 0) & (gh > 0), np.log(np.where(g2 > 0, g2, 1) / np.where(gh > 0, gh, 1)), 0.0)
+    want = f0 * np.exp((H.T @ u) / H.sum(axis=0))
+    assert np.allclose(oracle_lib.smart(geom2, taps2, g2, f0, 1), want, rtol=1e-13, atol=0)
+
+
+def test_smart_single_unit_tap_is_exact_in_one_step(oracle_lib):
+    """w = 1, one unit tap (H a selection): SMART reproduces the data in one step, f = E^T g."""
+    geom = syn.Geometry(5, 4, 1, 9, 8)
+    off = 2 + 9 * 3
+    taps = syn.Taps(np.array([0, 1]), np.array([off]), np.ones(1, np.float32))
+    ft = syn.scene_random(geom, seed=3, lo=0.5, hi=1.5)
+    g = oracle_lib.forward(geom, taps, ft)
+    f = oracle_lib.smart(geom, taps, g, np.ones(geom.m), 1)
+    assert np.max(np.abs(f - ft.reshape(-1))) <= 1e-12
