@@ -168,6 +168,15 @@ CTIS_API ctis_status ctis_back_update(ctis_plan plan, const float* r, float* f, 
 CTIS_API ctis_status ctis_back_update_from_ghat(ctis_plan plan, const float* g, const float* g_hat, float* f,
                                        void* ws, ctis_stream stream);
 
+/* SMART, the simultaneous form of the MART solver on the
+ * same projector, testing the paper's "solver agnostic" claim:
+ *   g_hat = H f;  r_p = log(g_p / g_hat_p) where g_p > 0 and g_hat_p > 0, else 0;
+ *   f <- f (.) exp( (H^T r) (/) h )
+ * `frames` >= 1 independent frames g[frames][n], f[frames][m] in place; ws as ctis_mlem_batched;
+ * iters = 0 leaves f unchanged.  Errors as ctis_mlem_batched. */
+CTIS_API ctis_status ctis_smart(ctis_plan plan, const float* g, float* f, int64_t frames, int iters, void* ws,
+                                ctis_stream stream);
+
 /* MLEM with the per-iteration Poisson log-likelihood and an early stop (the paper
  * recommends stopping early after Hagen; L is the objective EM ascends, shepp1982maximum):
  *   iteration k (k = 1, 2, ...): g_hat = H f^(k); ll[k-1] = L_k = sum_p [g_p log g_hat_p - g_hat_p]

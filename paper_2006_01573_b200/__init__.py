@@ -42,6 +42,7 @@ _SIGS = {
     "ctis_sensitivity": ([_P, _P, _P], _int),
     "ctis_mlem": ([_P, _P, _P, _int, _P, _P], _int),
     "ctis_mlem_batched": ([_P, _P, _P, _i64, _int, _P, _P], _int),
+    "ctis_smart": ([_P, _P, _P, _i64, _int, _P, _P], _int),
     "ctis_mlem_monitored": ([_P, _P, _P, _int, ctypes.c_double, _P, _P, _P, _P], _int),
     "ctis_back_update_from_ghat": ([_P, _P, _P, _P, _P, _P], _int),
     "ctis_forward_ratio": ([_P, _P, _P, _P, _P], _int),
@@ -212,6 +213,14 @@ class Plan:
         else:
             _check(_lib.ctis_mlem_batched(self._h, gp, fp, frames, int(iters), ctypes.c_void_p(ws.data_ptr()),
                                           _stream_handle(stream)), "ctis_mlem_batched")
+        return f
+
+    def smart(self, g, f, iters: int, ws=None, stream=None):
+        """In-place SMART (simultaneous MART, ctis_smart): f <- f exp(H^T log(g / Hf) / h), `iters` times."""
+        frames = g.numel() // self.n
+        ws = self.workspace(frames) if ws is None else ws
+        _check(_lib.ctis_smart(self._h, _dev_ptr(g, self.n * frames, "g"), _dev_ptr(f, self.m * frames, "f"), frames,
+                               int(iters), ctypes.c_void_p(ws.data_ptr()), _stream_handle(stream)), "ctis_smart")
         return f
 
     def mlem_monitored(self, g, f, max_iters: int, rel_tol: float = 0.0, ws=None, stream=None):

@@ -63,8 +63,9 @@ struct GraphKey {
   void* ws;
   int64_t frames;
   int iters;
+  int solver;  // 0 MLEM, 1 SMART
   bool operator<(const GraphKey& o) const {
-    return std::tie(g, f, ws, frames, iters) < std::tie(o.g, o.f, o.ws, o.frames, o.iters);
+    return std::tie(g, f, ws, frames, iters, solver) < std::tie(o.g, o.f, o.ws, o.frames, o.iters, o.solver);
   }
 };
 
@@ -957,7 +958,7 @@ ctis_status validate_data(ctis_plan_s& P, const float* g, const float* f, int64_
 
 // One MLEM reconstruction: ws = [A: g_hat accumulator, frames*n][B: r, frames*n].
 cudaError_t enqueue_mlem(ctis_plan_s& P, const float* g, float* f, float* ws, int frames, int iters, cudaStream_t s,
-                         int64_t* cnt) {
+                         int64_t* cnt, int solver = 0) {
   float* A = ws;
   float* B = ws + (((size_t)P.n * frames + 3) & ~(size_t)3);  // 16-byte aligned second half
   const long long count = (long long)P.n * frames;
@@ -965,15 +966,16 @@ cudaError_t enqueue_mlem(ctis_plan_s& P, const float* g, float* f, float* ws, in
   for (int k = 0; k < iters && e == cudaSuccess; ++k) {
     e = enqueue_forward(P, f, A, frames, s, cnt);
     if (e == cudaSuccess) {
-      e = launch_ratio(g, A, B, count, /*zero_ghat=*/true, s);
+      e = solver == 1 ? launch_log_ratio(g, A, B, count, s) : launch_ratio(g, A, B, count, /*zero_ghat=*/true, s);
       ++*cnt;
     }
-    if (e == cudaSuccess) e = enqueue_back(P, B, f, frames, 1, s, cnt);
+    if (e == cudaSuccess) e = enqueue_back(P, B, f, frames, solver == 1 ? 2 : 1, s, cnt);
   }
   return e;
 }
 
-ctis_status run_mlem(ctis_plan_s& P, const float* g, float* f, int64_t frames, int iters, void* ws, cudaStream_t s) {
+ctis_status run_mlem(ctis_plan_s& P, const float* g, float* f, int64_t frames, int iters, void* ws, cudaStream_t s,
+                     int solver = 0) {
   if (P.shard)
     return fail(CTIS_ERR_INVALID_ARGUMENT,
                 "mlem on a shard plan needs the collective: use ctis_forward + all-reduce + ctis_back_update_from_ghat");
@@ -991,11 +993,11 @@ ctis_status run_mlem(ctis_plan_s& P, const float* g, float* f, int64_t frames, i
   float* w = static_cast<float*>(ws);
   int64_t cnt = 0;
   if (!P.use_graph) {
-    CTIS_CUDA(enqueue_mlem(P, g, f, w, (int)frames, iters, s, &cnt), "mlem launch");
+    CTIS_CUDA(enqueue_mlem(P, g, f, w, (int)frames, iters, s, &cnt, solver), "mlem launch");
     P.last_launches += cnt;
     return CTIS_OK;
   }
-  GraphKey key{g, f, ws, frames, iters};
+  GraphKey key{g, f, ws, frames, iters, solver};
   auto it = P.graphs.find(key);
   if (it == P.graphs.end()) {
     if (P.graphs.size() >= 16) {
@@ -1004,7 +1006,7 @@ ctis_status run_mlem(ctis_plan_s& P, const float* g, float* f, int64_t frames, i
     }
     cudaGraph_t graph = nullptr;
     CTIS_CUDA(cudaStreamBeginCapture(P.side, cudaStreamCaptureModeThreadLocal), "begin capture");
-    cudaError_t e = enqueue_mlem(P, g, f, w, (int)frames, iters, P.side, &cnt);
+    cudaError_t e = enqueue_mlem(P, g, f, w, (int)frames, iters, P.side, &cnt, solver);
     cudaError_t e2 = cudaStreamEndCapture(P.side, &graph);
     if (e != cudaSuccess) {
       if (graph) cudaGraphDestroy(graph);
@@ -1276,6 +1278,13 @@ ctis_status ctis_mlem_batched(ctis_plan p, const float* g, float* f, int64_t fra
   if (!p) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL plan");
   std::lock_guard<std::mutex> lk(p->mu);
   return run_mlem(*p, g, f, frames, iters, ws, (cudaStream_t)stream);
+}
+
+ctis_status ctis_smart(ctis_plan p, const float* g, float* f, int64_t frames, int iters, void* ws,
+                       ctis_stream stream) {
+  if (!p) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL plan");
+  std::lock_guard<std::mutex> lk(p->mu);
+  return run_mlem(*p, g, f, frames, iters, ws, (cudaStream_t)stream, /*solver=*/1);
 }
 
 ctis_status ctis_mlem_monitored(ctis_plan p, const float* g, float* f, int max_iters, double rel_tol, void* ws,

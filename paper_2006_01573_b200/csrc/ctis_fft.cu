@@ -65,7 +65,8 @@ __global__ void fft_conj_mul_kernel(const cufftComplex* __restrict__ d, const cu
   }
 }
 
-// zeta_j = y_i[E(q)] / n (Eq. 15); mode 1: f_j <- f_j * zeta_j * (1/h_i), mode 0: out_j = zeta_j
+// zeta_j = y_i[E(q)] / n (Eq. 15); mode 1: f_j <- f_j * zeta_j * (1/h_i); 2: f_j <- f_j exp(zeta_j / h_i);
+// mode 0: out_j = zeta_j
 __global__ void fft_extract_kernel(const float* __restrict__ y, float* __restrict__ fz,
                                    const float* __restrict__ inv_h, int mode, int a, int gamma, long long n,
                                    long long ell, long long m, float inv_n) {
@@ -73,7 +74,8 @@ __global__ void fft_extract_kernel(const float* __restrict__ y, float* __restric
     const long long i = j / ell, q = j - i * ell;
     const long long qr = q % a, qc = q / a;
     const float z = y[i * n + qr + (long long)gamma * qc] * inv_n;
-    fz[j] = mode ? fz[j] * z * __ldg(inv_h + i) : z;
+    const float ih = __ldg(inv_h + i);
+    fz[j] = mode == 1 ? fz[j] * z * ih : mode == 2 ? fz[j] * expf(z * ih) : z;
   }
 }
 

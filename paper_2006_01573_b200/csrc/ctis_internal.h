@@ -70,7 +70,7 @@ struct TabArgs {
   long long src_frame; // elements between frames in src
   long long dst_frame; // elements between frames in dst
   int a, alpha, gamma, xi, n, ell;
-  int mode;            // back: 1 = update f in place, 0 = write z
+  int mode;            // back: 0 = write z, 1 = MLEM update of f in place, 2 = SMART update
   unsigned bias;       // forward: multiple of n with E(u) + bias >= 0 for every u of the u-space
   int nsub;            // forward: E(u) + bias + o_ref < (nsub + 1) * n
   int slot_floats;     // floats per pipeline slot (multiple of 32)

@@ -72,6 +72,23 @@ cudaError_t launch_validate(const float* x, long long count, int* flag, cudaStre
   return cudaGetLastError();
 }
 
+// SMART log-ratio r_p = log(g_p / g_hat_p) where both are > 0, else 0 (R17); resets g_hat.
+__global__ void log_ratio_kernel(const float* __restrict__ g, float* gh, float* r, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float gv = __ldg(g + i), hv = gh[i];
+    r[i] = (gv > 0.f && hv > 0.f) ? logf(__fdiv_rn(gv, hv)) : 0.f;
+    gh[i] = 0.f;
+  }
+}
+
+cudaError_t launch_log_ratio(const float* g, float* ghat, float* r, long long count, cudaStream_t s) {
+  const long long want = (count + 255) / 256;
+  const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
+  log_ratio_kernel<<<blocks, 256, 0, s>>>(g, ghat, r, count);
+  return cudaGetLastError();
+}
+
 // Ratio + Poisson log-likelihood of the current model (R15): each thread accumulates its
 // terms in fp64, the block reduces them (warp shuffles, then shared memory) and adds one value to
 // ll[*counter] with a double-precision atomic.

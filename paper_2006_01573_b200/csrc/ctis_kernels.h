@@ -7,6 +7,8 @@ namespace ctis {
 cudaError_t launch_ratio(const float* g, float* ghat, float* r, long long count, bool zero_ghat, cudaStream_t s);
 cudaError_t launch_sensitivity(const float* hband, float* h, int ell, int m, cudaStream_t s);
 cudaError_t launch_validate(const float* x, long long count, int* flag, cudaStream_t s);
+// SMART log-ratio (zeroing g_hat)
+cudaError_t launch_log_ratio(const float* g, float* ghat, float* r, long long count, cudaStream_t s);
 // ratio (zeroing g_hat) + ll[*counter] += sum_p [g log g_hat - g_hat] (fp64)
 cudaError_t launch_ratio_ll(const float* g, float* ghat, float* r, long long count, double* ll, const int* counter,
                             cudaStream_t s);

@@ -60,6 +60,12 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 __device__ __forceinline__ int tabi(uint32_t i) { return (int)c_tab[i]; }
+
+// Back-projection epilogue (TabArgs::mode): 0 z = H^T r; 1 MLEM f <- f * z / h (Eq. 2, Alg. 1 l. 12);
+// 2 SMART f <- f * exp(z / h) with r the log-ratio (R17)
+__device__ __forceinline__ float upd_value(int mode, float f, float z, float ih) {
+  return mode == 1 ? f * z * ih : mode == 2 ? f * expf(z * ih) : z;
+}
 __device__ __forceinline__ float tabf(uint32_t i) { return __uint_as_float(c_tab[i]); }
 
 __device__ __forceinline__ float lds(unsigned addr) {
@@ -472,11 +478,11 @@ __device__ __forceinline__ void back_body(const TabArgs& A, const CUtensorMap* t
       const float z1 = (b & 1) ? acc1[b >> 1].y : acc1[b >> 1].x;
       if (qc0 < A.alpha) {
         float* p = f + lb + (long long)A.a * qc0;
-        *p = A.mode ? (*p) * z0 * ih : z0;
+        *p = upd_value(A.mode, *p, z0, ih);
       }
       if (qc1 < A.alpha) {
         float* p = f + lb + (long long)A.a * qc1;
-        *p = A.mode ? (*p) * z1 * ih : z1;
+        *p = upd_value(A.mode, *p, z1, ih);
       }
     }
   }
@@ -877,11 +883,11 @@ __device__ __forceinline__ void back_persistent(const TabArgs& A, const CUtensor
           const float z1 = (b & 1) ? acc1[b >> 1].y : acc1[b >> 1].x;
           if (qc0 < A.alpha) {
             float* p = f + lb + (long long)A.a * qc0;
-            *p = A.mode ? (*p) * z0 * ih : z0;
+            *p = upd_value(A.mode, *p, z0, ih);
           }
           if (qc1 < A.alpha) {
             float* p = f + lb + (long long)A.a * qc1;
-            *p = A.mode ? (*p) * z1 * ih : z1;
+            *p = upd_value(A.mode, *p, z1, ih);
           }
         }
       }
@@ -1030,7 +1036,7 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
           for (int k4 = 0; k4 < 4; ++k4) {
             const int qc = q_c0 + warp + NWARPS * k4;
             const float zz = (b & 1) ? acc[k4][b >> 1].y : acc[k4][b >> 1].x;
-            if (qc < A.alpha) f[lb + (long long)A.a * qc] = A.mode ? old[k4] * zz * ih : zz;
+            if (qc < A.alpha) f[lb + (long long)A.a * qc] = upd_value(A.mode, old[k4], zz, ih);
           }
         }
       }

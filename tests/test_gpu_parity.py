@@ -383,3 +383,32 @@ def test_fft_projector_wrapping_taps_and_switch_back(ctis, oracle_lib, dev):
         fd = torch.ones(geom.m, dtype=torch.float32, device=dev)
         plan.mlem(cuda(g, dev), fd, 10)
         assert rel(fd.cpu().numpy(), oracle_lib.mlem(geom, taps, g, np.ones(geom.m), 10)) <= MLEM_TOL
+
+
+# ------------------------------------------------------------------ §8(f) f-4: SMART on the same projector
+@pytest.mark.parametrize("name", ["tiny", "C2", "C3"])
+def test_smart_vs_oracle(ctis, oracle_lib, dev, name):
+    cfg = syn.config(name)
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    K = min(cfg.K, 30)
+    g = oracle_lib.forward(geom, taps, syn.scene_blobs(geom)).astype(np.float32)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    fd = torch.ones(geom.m, dtype=torch.float32, device=dev)
+    plan.smart(cuda(g, dev), fd, K)
+    assert rel(fd.cpu().numpy(), oracle_lib.smart(geom, taps, g, np.ones(geom.m), K)) <= MLEM_TOL
+
+
+def test_smart_wrapping_batched_and_fft_projector(ctis, oracle_lib, dev):
+    """Wrapping taps (element-loader kernels), two frames in one call, and the Fourier projector."""
+    geom = syn.Geometry(33, 17, 6, 70, 45)
+    taps = syn.random_taps(geom, (2, 9), seed=77, region="any")
+    gs = [oracle_lib.forward(geom, taps, syn.scene_random(geom, seed=s, lo=0.1, zero_frac=0.1)).astype(np.float32)
+          for s in (3, 4)]
+    want = [oracle_lib.smart(geom, taps, g, np.ones(geom.m), 12) for g in gs]
+    plan = ctis.Plan.from_geometry(geom, taps)
+    for proj in (0, 1):
+        plan.set_option(ctis.OPT_PROJECTOR, proj)
+        fd = torch.ones((2, geom.m), dtype=torch.float32, device=dev)
+        plan.smart(torch.from_numpy(np.stack(gs)).to(dev), fd, 12)
+        for i in range(2):
+            assert rel(fd[i].cpu().numpy(), want[i]) <= MLEM_TOL
