@@ -570,6 +570,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
       if (occ == 3 && mm > 24) occ = 2;
       if (occ < 2 || occ > 4) occ = 2;
       P.fwd_g = occ;
+
       P.fwd_m = mm;
       maxm = mm;
     } else {
@@ -829,6 +830,16 @@ ctis_status check_frames(int64_t frames) {
 }
 
 // ---- launches --------------------------------------------------------------------------------
+// Programmatic dependent launches between the MLEM kernels: off by default (CTIS_PDL=1 enables) —
+// measured slower on B200 (C4 150.0 -> 155.2 us/iteration, C3 40.8 -> 46.9: tools/mlem_time.py).
+bool pdl_enabled() {
+  static bool v = [] {
+    const char* e = std::getenv("CTIS_PDL");
+    return e && std::atoi(e) == 1;
+  }();
+  return v;
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no link against libcuda).
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -871,6 +882,22 @@ cudaError_t make_tensor_map(CUtensorMap* tm, bool forward, const ctis_plan_s& P,
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may start while its predecessor
+// drains; it waits for the predecessor's results with griddepcontrol.wait (ctis_tables.cu pdl_enter).
+cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 int debug_flags() {
   static int v = [] {
     const char* e = std::getenv("CTIS_DEBUG");
@@ -910,11 +937,11 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
     // TMA kernels are persistent (2 CTAs per SM walk the page's items); element-loader kernels are
     // one CTA per (tile, chunk, frame)
     const long long items = (long long)pg.total_items * frames;
-    const int per_sm = (fwd && P.fwd_g >= 2) ? P.fwd_g : 2;
+    const int per_sm = fwd ? (P.fwd_g == 3 ? 3 : P.fwd_g == 4 ? 4 : 2) : 2;  // resident CTAs per SM
     dim3 grid = tma ? dim3((unsigned)std::min<long long>(items, (long long)per_sm * P.sms), 1, 1)
                     : dim3(pg.max_tiles, pg.nchunks, frames);
     void* args[] = {&A, &tm};
-    cudaError_t e = cudaLaunchKernel((const void*)pg.kern, grid, dim3(threads), args, smem, s);
+    cudaError_t e = launch_pdl((const void*)pg.kern, grid, dim3(threads), args, smem, s);
     if (e != cudaSuccess) return e;
     if (count) ++*count;
   }
@@ -966,7 +993,8 @@ cudaError_t enqueue_mlem(ctis_plan_s& P, const float* g, float* f, float* ws, in
   for (int k = 0; k < iters && e == cudaSuccess; ++k) {
     e = enqueue_forward(P, f, A, frames, s, cnt);
     if (e == cudaSuccess) {
-      e = solver == 1 ? launch_log_ratio(g, A, B, count, s) : launch_ratio(g, A, B, count, /*zero_ghat=*/true, s);
+      e = solver == 1 ? launch_log_ratio(g, A, B, count, s, pdl_enabled())
+                      : launch_ratio(g, A, B, count, /*zero_ghat=*/true, s, pdl_enabled());
       ++*cnt;
     }
     if (e == cudaSuccess) e = enqueue_back(P, B, f, frames, solver == 1 ? 2 : 1, s, cnt);
@@ -1102,7 +1130,7 @@ ctis_status run_mlem_monitored(ctis_plan_s& P, const float* g, float* f, int max
     if (e != cudaSuccess) return bail(e, "capture to WHILE body");
     cudaError_t e1 = enqueue_forward(P, f, A, 1, P.side, &body_launches);
     if (e1 == cudaSuccess) {
-      e1 = launch_ratio_ll(g, A, B, P.n, ll, cnt, P.side);
+      e1 = launch_ratio_ll(g, A, B, P.n, ll, cnt, P.side, pdl_enabled());
       ++body_launches;
     }
     if (e1 == cudaSuccess) e1 = enqueue_back(P, B, f, 1, 1, P.side, &body_launches);

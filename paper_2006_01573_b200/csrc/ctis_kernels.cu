@@ -10,10 +10,32 @@
 
 namespace ctis {
 
+// Programmatic dependent launch (see ctis_tables.cu pdl_enter)
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... Args>
+cudaError_t launch_ex(void (*kern)(Args...), int blocks, int threads, cudaStream_t s, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // Ratio over `count` pixels; if zero_ghat, g_hat is reset to 0 after it is read (so the next
 // forward projection can accumulate into it with red.add).  Vectorised by 4 when aligned.
 __global__ void ratio_kernel(const float* __restrict__ g, float* gh, float* r,
                              long long count, int zero_ghat) {
+  pdl_enter();
   const bool aligned = ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(gh) |
                          reinterpret_cast<uintptr_t>(r)) & 15u) == 0;
   const long long n4 = aligned ? (count >> 2) : 0;
@@ -37,11 +59,11 @@ __global__ void ratio_kernel(const float* __restrict__ g, float* gh, float* r,
   }
 }
 
-cudaError_t launch_ratio(const float* g, float* ghat, float* r, long long count, bool zero_ghat, cudaStream_t s) {
+cudaError_t launch_ratio(const float* g, float* ghat, float* r, long long count, bool zero_ghat, cudaStream_t s,
+                         bool pdl) {
   const long long want = (count / 4 + 255) / 256;
   const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
-  ratio_kernel<<<blocks, 256, 0, s>>>(g, ghat, r, count, zero_ghat ? 1 : 0);
-  return cudaGetLastError();
+  return launch_ex(ratio_kernel, blocks, 256, s, pdl, g, ghat, r, count, zero_ghat ? 1 : 0);
 }
 
 __global__ void sensitivity_kernel(const float* __restrict__ hband, float* __restrict__ h, int ell, int m) {
@@ -74,6 +96,7 @@ cudaError_t launch_validate(const float* x, long long count, int* flag, cudaStre
 
 // SMART log-ratio r_p = log(g_p / g_hat_p) where both are > 0, else 0 (R17); resets g_hat.
 __global__ void log_ratio_kernel(const float* __restrict__ g, float* gh, float* r, long long count) {
+  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
        i += (long long)gridDim.x * blockDim.x) {
     const float gv = __ldg(g + i), hv = gh[i];
@@ -82,11 +105,10 @@ __global__ void log_ratio_kernel(const float* __restrict__ g, float* gh, float* 
   }
 }
 
-cudaError_t launch_log_ratio(const float* g, float* ghat, float* r, long long count, cudaStream_t s) {
+cudaError_t launch_log_ratio(const float* g, float* ghat, float* r, long long count, cudaStream_t s, bool pdl) {
   const long long want = (count + 255) / 256;
   const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
-  log_ratio_kernel<<<blocks, 256, 0, s>>>(g, ghat, r, count);
-  return cudaGetLastError();
+  return launch_ex(log_ratio_kernel, blocks, 256, s, pdl, g, ghat, r, count);
 }
 
 // Ratio + Poisson log-likelihood of the current model (R15): each thread accumulates its
@@ -94,6 +116,7 @@ cudaError_t launch_log_ratio(const float* g, float* ghat, float* r, long long co
 // ll[*counter] with a double-precision atomic.
 __global__ void ratio_ll_kernel(const float* __restrict__ g, float* gh, float* r, long long count, double* ll,
                                 const int* __restrict__ counter) {
+  pdl_enter();
   const long long stride = (long long)gridDim.x * blockDim.x;
   double acc = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += stride) {
@@ -120,11 +143,10 @@ __global__ void ratio_ll_kernel(const float* __restrict__ g, float* gh, float* r
 }
 
 cudaError_t launch_ratio_ll(const float* g, float* ghat, float* r, long long count, double* ll, const int* counter,
-                            cudaStream_t s) {
+                            cudaStream_t s, bool pdl) {
   const long long want = (count + 255) / 256;
   const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
-  ratio_ll_kernel<<<blocks, 256, 0, s>>>(g, ghat, r, count, ll, counter);
-  return cudaGetLastError();
+  return launch_ex(ratio_ll_kernel, blocks, 256, s, pdl, g, ghat, r, count, ll, counter);
 }
 
 // Stop rule after update k = *counter + 1 (R16), evaluated on the device: sets the WHILE

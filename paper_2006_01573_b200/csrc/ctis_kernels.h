@@ -4,14 +4,16 @@
 #include <cuda_runtime.h>
 
 namespace ctis {
-cudaError_t launch_ratio(const float* g, float* ghat, float* r, long long count, bool zero_ghat, cudaStream_t s);
+// pdl: launch with programmatic stream serialization (the kernels call griddepcontrol.wait first)
+cudaError_t launch_ratio(const float* g, float* ghat, float* r, long long count, bool zero_ghat, cudaStream_t s,
+                         bool pdl = false);
 cudaError_t launch_sensitivity(const float* hband, float* h, int ell, int m, cudaStream_t s);
 cudaError_t launch_validate(const float* x, long long count, int* flag, cudaStream_t s);
 // SMART log-ratio (zeroing g_hat)
-cudaError_t launch_log_ratio(const float* g, float* ghat, float* r, long long count, cudaStream_t s);
+cudaError_t launch_log_ratio(const float* g, float* ghat, float* r, long long count, cudaStream_t s, bool pdl = false);
 // ratio (zeroing g_hat) + ll[*counter] += sum_p [g log g_hat - g_hat] (fp64)
 cudaError_t launch_ratio_ll(const float* g, float* ghat, float* r, long long count, double* ll, const int* counter,
-                            cudaStream_t s);
+                            cudaStream_t s, bool pdl = false);
 // one thread: ++*counter, then the WHILE condition (continue unless max_iters or the stop rule)
 cudaError_t launch_mlem_check(const double* ll, int* counter, int max_iters, double rel_tol,
                               unsigned long long cond_handle, cudaStream_t s);

@@ -95,6 +95,18 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+// non-blocking probe of an mbarrier phase (true once the phase with this parity has completed)
+__device__ __forceinline__ bool mbar_test(unsigned bar, unsigned parity) {
+  unsigned r;
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(r)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return r != 0;
+}
 __device__ __forceinline__ unsigned atom_add_shared(unsigned addr, unsigned v) {
   unsigned old;
   asm volatile("atom.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
@@ -638,7 +650,7 @@ __device__ __forceinline__ void red_nz(float* p, float v) {
       : "memory");
 }
 
-template <int MAXM, int S>
+template <int MAXM, int S, bool EARLY>
 __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUtensorMap* tm) {
   extern __shared__ __align__(128) float smem[];
   constexpr int K = S / 2, MP = MAXM / 2;
@@ -698,6 +710,7 @@ __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUte
   const unsigned tb1 = tb0 + 4u * A.box_r * NW;
   const unsigned n = (unsigned)A.n;
   unsigned w = 0, next_refill = K;
+  bool ready = false;  // the current window's full barrier was already seen complete (early probe)
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
     int z, k, tile;
     decode_item(it, per_frame, nch, z, k, tile);
@@ -729,12 +742,15 @@ __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUte
         }
         next_refill = w + K;
       }
-      if (!(A.dbg & 1)) mbar_wait(full + 8 * c_slot, c_phase);
+      if (!(A.dbg & 1) && !ready) mbar_wait(full + 8 * c_slot, c_phase);
+      // probe the next window's barrier now: its latency overlaps this band's tap loop, and the next
+      // trip skips the blocking wait when the window had already landed
+      const unsigned n_slot = c_slot + 1 == S ? 0u : c_slot + 1, n_phase = c_slot + 1 == S ? c_phase ^ 1u : c_phase;
+      const bool ready_next = EARLY && mbar_test(full + 8 * n_slot, n_phase);
       compute(c_slot * slot_bytes, b);
-      if (++c_slot == S) {
-        c_slot = 0;
-        c_phase ^= 1u;
-      }
+      c_slot = n_slot;
+      c_phase = n_phase;
+      ready = ready_next;
     }
     // flush this item: g_hat[(E(u) + o_ref) mod n] += acc for both positions (see forward_group)
     float* g = A.dst + (long long)z * A.dst_frame;
@@ -895,6 +911,14 @@ __device__ __forceinline__ void back_persistent(const TabArgs& A, const CUtensor
   }
 }
 
+// Programmatic dependent launch: let the next kernel of the MLEM chain be scheduled as soon as this
+// grid's CTAs are all resident, and wait for the previous kernel's results (its memory is visible
+// after griddepcontrol.wait) — hides the kernel-boundary launch latency inside the CUDA graph.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // CTIS_DEBUG & 8: fill the window ring with NaN before the kernel runs, so that any read of shared
 // memory the kernel did not write this launch poisons the result (tests/test_gpu_parity.py)
 __device__ __forceinline__ void nan_fill_smem(int nf) {
@@ -1050,12 +1074,14 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
   extern "C" __global__ void __launch_bounds__(kFwdThreads, MINB)                                          \
       ctis_fwd_g1_m##M##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                      \
     if (A.frames == 0) return;                                                                             \
+    pdl_enter();                                                                                           \
     if (A.dbg & 8) nan_fill_smem(kFwdStages * A.slot_floats);                                                  \
     forward_persistent<M>(A, &tm);                                                                         \
   }                                                                                                        \
   extern "C" __global__ void __launch_bounds__(kFwdThreads, MINB)                                          \
       ctis_fwd_g1_m##M##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                      \
     if (A.frames == 0) return;                                                                             \
+    pdl_enter();                                                                                           \
     if (A.dbg & 8) nan_fill_smem(kFwdStages * A.slot_floats);                                                  \
     forward_body<1, M, false, true>(A, &tm);                                                               \
   }
@@ -1088,8 +1114,9 @@ CTIS_FWD(96, 1)
   extern "C" __global__ void __launch_bounds__(kFwd2Threads, OCC)                                          \
       ctis_fwd_g##OCC##_m##M##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                \
     if (A.frames == 0) return;                                                                             \
+    pdl_enter();                                                                                           \
     if (A.dbg & 8) nan_fill_smem(S * A.slot_floats);                                                           \
-    forward_persistent2<M, S>(A, &tm);                                                                     \
+    forward_persistent2<M, S, true>(A, &tm);                                                                     \
   }
 CTIS_FWD2(2, 8, 2)
 CTIS_FWD2(2, 8, 4)
@@ -1134,6 +1161,7 @@ CTIS_FWD2(4, 4, 16)
   extern "C" __global__ void __launch_bounds__(kBack4Threads, 2)                                           \
       ctis_back4_b##NB##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                      \
     if (A.frames == 0) return;                                                                             \
+    pdl_enter();                                                                                           \
     if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                             \
     back_persistent4<NB>(A, &tm);                                                                          \
   }
@@ -1147,12 +1175,14 @@ CTIS_BACK4(16)
   extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
       ctis_back_b##NB##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                       \
     if (A.frames == 0) return;                                                                             \
+    pdl_enter();                                                                                           \
     if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                                 \
     back_persistent<NB>(A, &tm);                                                                     \
   }                                                                                                        \
   extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
       ctis_back_b##NB##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                       \
     if (A.frames == 0) return;                                                                             \
+    pdl_enter();                                                                                           \
     if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                                 \
     back_body<NB, false, true>(A, &tm);                                                                    \
   }
