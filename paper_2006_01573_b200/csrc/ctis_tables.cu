@@ -1041,26 +1041,40 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
         c += 1;
       }
     }
-    // epilogue of this item: f <- f * z * (1/h_lam) (or z); all loads of f first, then the stores
+    // epilogue of this item: f <- f * z * (1/h_lam) (or z).  Loads of f for groups of EG bands are
+    // issued together (ld.global.nc: each element is read and then written by this thread only), then
+    // the stores: one L2 round trip per group instead of one per band (the compiler cannot move a
+    // band's loads above the previous band's stores to the same array)
     float* f = A.dst + (long long)z * A.dst_frame;
     const int qr = q_r0 + lane;
+    constexpr int EG = NB < 6 ? NB : 6;
     if (qr < A.a) {
 #pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        if (b < nb) {
-          const long long lb = (long long)(lam0 + b) * A.ell + qr;
-          const float ih = tabf(IH + b);
-          float old[4];
+      for (int b0 = 0; b0 < NB; b0 += EG) {
+        float old[EG][4];
+#pragma unroll
+        for (int bb = 0; bb < EG; ++bb) {
+          const int b = b0 + bb;
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
             const int qc = q_c0 + warp + NWARPS * k4;
-            old[k4] = (A.mode && qc < A.alpha) ? f[lb + (long long)A.a * qc] : 1.f;
+            old[bb][k4] = 1.f;
+            if (b < NB && b < nb && A.mode && qc < A.alpha)
+              old[bb][k4] = __ldg(f + (long long)(lam0 + b) * A.ell + qr + (long long)A.a * qc);
           }
+        }
 #pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4) {
-            const int qc = q_c0 + warp + NWARPS * k4;
-            const float zz = (b & 1) ? acc[k4][b >> 1].y : acc[k4][b >> 1].x;
-            if (qc < A.alpha) f[lb + (long long)A.a * qc] = upd_value(A.mode, old[k4], zz, ih);
+        for (int bb = 0; bb < EG; ++bb) {
+          const int b = b0 + bb;
+          if (b < NB && b < nb) {
+            const long long lb = (long long)(lam0 + b) * A.ell + qr;
+            const float ih = tabf(IH + b);
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const int qc = q_c0 + warp + NWARPS * k4;
+              const float zz = (b & 1) ? acc[k4][b >> 1].y : acc[k4][b >> 1].x;
+              if (qc < A.alpha) f[lb + (long long)A.a * qc] = upd_value(A.mode, old[bb][k4], zz, ih);
+            }
           }
         }
       }

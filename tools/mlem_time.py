@@ -27,4 +27,4 @@ for _ in range(15):
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b) * 1e3 / K)
 ts.sort()
-print(f"{name} pdl={os.environ.get('CTIS_PDL', '1')} us/iter min {ts[0]:.1f} med {ts[len(ts) // 2]:.1f} max {ts[-1]:.1f}")
+print(f"{name} pdl={os.environ.get('CTIS_PDL', '0')} us/iter min {ts[0]:.1f} med {ts[len(ts) // 2]:.1f} max {ts[-1]:.1f}")
