@@ -600,7 +600,7 @@ __device__ __forceinline__ void forward_persistent(const TabArgs& A, const CUten
         __syncthreads();  // every warp has consumed the windows before w: their slots are free
         if (threadIdx.x == 0) {
 #pragma unroll
-          for (int q = 0; q < K; ++q)
+          for (int q = 0; q < S; ++q)  // catch up fully: refill points can land one window late
             if (p_w < w + S) issue_one();
         }
         next_refill = w + K;
@@ -737,7 +737,7 @@ __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUte
         __syncthreads();  // every warp has consumed the windows before w: their slots are free
         if (threadIdx.x == 0 && !(A.dbg & 1)) {
 #pragma unroll 1
-          for (int q = 0; q < K; ++q)
+          for (int q = 0; q < S; ++q)  // catch up fully: refill points can land one window late
             if (p_w < w + S) issue_one();
         }
         next_refill = w + K;
@@ -867,7 +867,7 @@ __device__ __forceinline__ void back_persistent(const TabArgs& A, const CUtensor
         __syncthreads();
         if (threadIdx.x == 0) {
 #pragma unroll
-          for (int q = 0; q < K; ++q)
+          for (int q = 0; q < S; ++q)  // catch up fully: refill points can land one window late
             if (p_w < w + S) issue_one();
         }
         next_refill = w + K;
@@ -1022,7 +1022,7 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
         __syncthreads();
         if (threadIdx.x == 0) {
 #pragma unroll
-          for (int q = 0; q < K; ++q)
+          for (int q = 0; q < S; ++q)  // catch up fully: refill points can land one window late
             if (p_w < w + S) issue_one();
         }
         next_refill = w + K;

@@ -412,3 +412,20 @@ def test_smart_wrapping_batched_and_fft_projector(ctis, oracle_lib, dev):
         plan.smart(torch.from_numpy(np.stack(gs)).to(dev), fd, 12)
         for i in range(2):
             assert rel(fd[i].cpu().numpy(), want[i]) <= MLEM_TOL
+
+
+def test_batched_frames_many_items_per_cta(ctis, dev):
+    """8 frames of C3: every persistent CTA walks many work items, so the TMA ring's refill points
+    drift across items with an odd number of windows (a back-kernel deadlock once hid here)."""
+    cfg = syn.config("C3")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    F = 8
+    scenes = np.stack([syn.frame_scene(geom, i).reshape(-1) for i in range(F)])
+    g = plan.forward(cuda(scenes, dev).view(F, geom.m))
+    fb = torch.ones(F, geom.m, device=dev)
+    plan.mlem(g, fb, 5)
+    for i in (0, 5, 7):
+        fi = torch.ones(geom.m, device=dev)
+        plan.mlem(g[i].contiguous(), fi, 5)
+        assert rel(fi.cpu().numpy(), fb[i].cpu().numpy()) <= 1e-6
