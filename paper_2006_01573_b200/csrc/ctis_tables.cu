@@ -599,7 +599,7 @@ __device__ __forceinline__ void forward_persistent(const TabArgs& A, const CUten
       if (w >= next_refill) {
         __syncthreads();  // every warp has consumed the windows before w: their slots are free
         if (threadIdx.x == 0) {
-#pragma unroll
+#pragma unroll 1
           for (int q = 0; q < S; ++q)  // catch up fully: refill points can land one window late
             if (p_w < w + S) issue_one();
         }
@@ -866,7 +866,7 @@ __device__ __forceinline__ void back_persistent(const TabArgs& A, const CUtensor
       if (w >= next_refill) {
         __syncthreads();
         if (threadIdx.x == 0) {
-#pragma unroll
+#pragma unroll 1
           for (int q = 0; q < S; ++q)  // catch up fully: refill points can land one window late
             if (p_w < w + S) issue_one();
         }
@@ -1021,7 +1021,7 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
       if (w >= next_refill) {
         __syncthreads();
         if (threadIdx.x == 0) {
-#pragma unroll
+#pragma unroll 1
           for (int q = 0; q < S; ++q)  // catch up fully: refill points can land one window late
             if (p_w < w + S) issue_one();
         }
