@@ -91,6 +91,7 @@ struct Page {
   int max_tiles = 0;
   int max_modes = 0;
   int total_items = 0;  // tiles summed over the page's chunks (persistent kernels)
+  int back_tc = 32;     // back pages: tile columns (kernel family)
   std::vector<uint32_t> words;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
@@ -107,6 +108,7 @@ struct ctis_plan_s {
   bool shard = false, validate = true, use_graph = true;
   bool tma_f = false, tma_b = false;
   int back_nb = kBackBandsMax;
+  int back_tc = kBackTC;  // back tile columns: 32, or 16 for small TMA plans (ctis_back2_*)
   int fbox_r = 0, fbox_c = 0, bbox_r = 0, bbox_c = 0;
   int fwd_g = 1, fwd_m = 8;
   int sms = 148;
@@ -327,7 +329,7 @@ bool back_desc(const ctis_plan_s& P, int b0, int nb, int NB, const std::vector<M
                const std::vector<float>& invh, int box_r, int box_c, std::vector<uint32_t>& out, int& tiles) {
   const int nm = (int)ms.size();
   out.assign(kDescHeader + 4 * nm + 2 * nm * NB + ((nb + 3) & ~3), 0u);  // length % 4 == 0
-  const int tiles_r = (P.a + kBackTR - 1) / kBackTR, tiles_c = (P.alpha + kBackTC - 1) / kBackTC;
+  const int tiles_r = (P.a + kBackTR - 1) / kBackTR, tiles_c = (P.alpha + P.back_tc - 1) / P.back_tc;
   out[0] = (uint32_t)b0;
   out[1] = (uint32_t)nb;
   out[2] = (uint32_t)nm;
@@ -462,8 +464,8 @@ ctis_status load_page(Page& pg, bool vec) {
     name = "ctis_fwd_g" + std::to_string(pg.max_modes / 1000) + "_m" + std::to_string(pg.max_modes % 1000) +
            (vec ? "_t" : "_s");
   } else {
-    name = std::string(vec && back4_enabled() ? "ctis_back4_b" : "ctis_back_b") + std::to_string(pg.max_modes) +
-           (vec ? "_t" : "_s");
+    name = std::string(vec && back4_enabled() ? (pg.back_tc == 16 ? "ctis_back2_b" : "ctis_back4_b") : "ctis_back_b") +
+           std::to_string(pg.max_modes) + (vec ? "_t" : "_s");
   }
   CTIS_CUDA(cudaLibraryGetKernel(&pg.kern, pg.lib, name.c_str()), "cudaLibraryGetKernel");
   int dev = 0;
@@ -494,7 +496,7 @@ int choose_back_nb(const ctis_plan_s& P) {
     const int v = std::atoi(e);
     if (v == 2 || v == 4 || v == 8 || v == 12 || v == 16) return v;
   }
-  const long long tiles = (long long)((P.a + kBackTR - 1) / kBackTR) * ((P.alpha + kBackTC - 1) / kBackTC);
+  const long long tiles = (long long)((P.a + kBackTR - 1) / kBackTR) * ((P.alpha + P.back_tc - 1) / P.back_tc);
   const long long slots = 148LL * 2;
   int best = kBackBandsMax;
   double bestc = 1e300;
@@ -624,7 +626,20 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
   // ---- back: NB (kernel template) chosen so that tiles x chunks fills the SMs; a chunk whose
   //      descriptor would not fit one 64 KB page is split further
   {
+    P.back_tc = kBackTC;
+    bool allow16 = true;
+  back_layout:
     P.back_nb = choose_back_nb(P);
+    if (allow16) {  // small TMA plans: 32 x 16 tiles (two voxels per thread) when 32 x 32 tiles leave CTA slots idle
+      const long long t32 = (long long)((P.a + kBackTR - 1) / kBackTR) * ((P.alpha + kBackTC - 1) / kBackTC);
+      const char* e = std::getenv("CTIS_BACK_TC");
+      // measured: tiny 14.8 -> 13.3 us, C2 unchanged, C3 (208 items) 25.0 -> 25.2 us: only below one item per SM
+      const bool want16 = e ? std::atoi(e) == 16 : t32 * ((P.w + P.back_nb - 1) / P.back_nb) < (long long)P.sms;
+      if (want16 && P.tma_b && back4_enabled()) {
+        P.back_tc = 16;
+        P.back_nb = choose_back_nb(P);
+      }
+    }
     std::vector<std::pair<int, int>> todo = balanced_chunks(P.w, P.back_nb);
     std::vector<std::vector<Mode>> cms;
     for (auto [b0, nb] : todo) {
@@ -637,7 +652,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
         for (const Mode& md : ms) {
           const Span sp = mode_span(md);
           box_r = std::max(box_r, kBackTR + sp.rmax - sp.rmin + 3);
-          box_c = std::max(box_c, kBackTC + sp.cmax - sp.cmin);
+          box_c = std::max(box_c, P.back_tc + sp.cmax - sp.cmin);
         }
       box_r = std::max(4, round4(box_r));
       box_c = std::max(1, box_c);
@@ -647,7 +662,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     // The persistent TMA back kernel needs every window of every tile to be a plain FPA box (no
     // carry / wrap of Eq. 7); otherwise the plan uses the exact element-loader kernels.
     if (P.tma_b) {
-      const int tiles_r = (P.a + kBackTR - 1) / kBackTR, tiles_c = (P.alpha + kBackTC - 1) / kBackTC;
+      const int tiles_r = (P.a + kBackTR - 1) / kBackTR, tiles_c = (P.alpha + P.back_tc - 1) / P.back_tc;
       for (const auto& ms : cms) {
         for (const Mode& md : ms) {
           const Span sp = mode_span(md);
@@ -659,7 +674,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
           const int br = (int)(Bm % P.gamma), bc = (int)(Bm / P.gamma);
           for (int tc = 0; tc < tiles_c && P.tma_b; ++tc)
             for (int tr = 0; tr < tiles_r && P.tma_b; ++tr) {
-              int R0 = tr * kBackTR + br, C0 = tc * kBackTC + bc;
+              int R0 = tr * kBackTR + br, C0 = tc * P.back_tc + bc;
               if (R0 >= P.gamma) {
                 R0 -= P.gamma;
                 C0 += 1;
@@ -669,6 +684,11 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
             }
         }
       }
+    }
+    if (!P.tma_b && P.back_tc != kBackTC) {  // element-loader kernels use 32 x 32 tiles: lay out again
+      P.back_tc = kBackTC;
+      allow16 = false;
+      goto back_layout;
     }
     std::vector<std::vector<uint32_t>> descs;
     std::vector<int> tiles;
@@ -703,6 +723,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     if (st) return st;
   }
   for (Page& pg : P.back) {
+    pg.back_tc = P.back_tc;
     pg.pair = P.pair;
     ctis_status st = load_page(pg, P.tma_b);
     if (st) return st;

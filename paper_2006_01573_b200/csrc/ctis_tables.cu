@@ -929,8 +929,11 @@ __device__ __forceinline__ void nan_fill_smem(int nf) {
 
 // Back with four voxels per thread (columns warp + 8k of the 32 x 32 tile, 256 threads): every tap
 // entry read through the uniform datapath feeds eight shared-memory loads (cf. forward_persistent2).
-template <int NB>
+// POS voxels per thread: columns warp + 8k (k < POS) of a 32 x 8*POS tile (POS = 2 for small problems,
+// where 32 x 32 tiles would leave SMs idle)
+template <int NB, int POS>
 __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtensorMap* tm) {
+  constexpr int TC = 8 * POS;
   extern __shared__ __align__(128) float smem[];
   constexpr int S = kBackStages, K = S / 2, BP = NB / 2;
   constexpr int NWARPS = kBack4Threads / 32;  // 8: voxel columns warp + 8k, k < 4
@@ -964,7 +967,7 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
     const int tiles_r = tabi(D + 3);
     p_nm = tabi(D + 2);
     p_qr = (tile % tiles_r) * kBackTR;
-    p_qc = (tile / tiles_r) * kBackTC;
+    p_qc = (tile / tiles_r) * TC;
     p_MI = D + kDescHeader;
     p_mode = 0;
   };
@@ -997,11 +1000,11 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
     decode_item(it, per_frame, nch, z, k, tile);
     const uint32_t D = c_tab[1 + k];
     const int lam0 = tabi(D + 0), nb = tabi(D + 1), nm = tabi(D + 2), tiles_r = tabi(D + 3);
-    const int q_r0 = (tile % tiles_r) * kBackTR, q_c0 = (tile / tiles_r) * kBackTC;
+    const int q_r0 = (tile % tiles_r) * kBackTR, q_c0 = (tile / tiles_r) * TC;
     const uint32_t MI = D + kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * NB;
-    float2 acc[4][BP];
+    float2 acc[POS][BP];
 #pragma unroll
-    for (int k4 = 0; k4 < 4; ++k4)
+    for (int k4 = 0; k4 < POS; ++k4)
 #pragma unroll
       for (int q = 0; q < BP; ++q) acc[k4][q] = make_float2(0.f, 0.f);
     auto compute = [&](unsigned ba, int c) {
@@ -1011,7 +1014,7 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
         const uint4 e = ent[q];
         const float2 wv = make_float2(__uint_as_float(e.z), __uint_as_float(e.w));
 #pragma unroll
-        for (int k4 = 0; k4 < 4; ++k4) {
+        for (int k4 = 0; k4 < POS; ++k4) {
           const unsigned bk = ba + k4 * cstep;
           acc[k4][q] = __ffma2_rn(wv, make_float2(lds(bk + e.x), lds(bk + e.y)), acc[k4][q]);
         }
@@ -1051,12 +1054,12 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
     if (qr < A.a) {
 #pragma unroll
       for (int b0 = 0; b0 < NB; b0 += EG) {
-        float old[EG][4];
+        float old[EG][POS];
 #pragma unroll
         for (int bb = 0; bb < EG; ++bb) {
           const int b = b0 + bb;
 #pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4) {
+          for (int k4 = 0; k4 < POS; ++k4) {
             const int qc = q_c0 + warp + NWARPS * k4;
             old[bb][k4] = 1.f;
             if (b < NB && b < nb && A.mode && qc < A.alpha)
@@ -1070,7 +1073,7 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
             const long long lb = (long long)(lam0 + b) * A.ell + qr;
             const float ih = tabf(IH + b);
 #pragma unroll
-            for (int k4 = 0; k4 < 4; ++k4) {
+            for (int k4 = 0; k4 < POS; ++k4) {
               const int qc = q_c0 + warp + NWARPS * k4;
               const float zz = (b & 1) ? acc[k4][b >> 1].y : acc[k4][b >> 1].x;
               if (qc < A.alpha) f[lb + (long long)A.a * qc] = upd_value(A.mode, old[bb][k4], zz, ih);
@@ -1171,19 +1174,23 @@ CTIS_FWD2(4, 4, 12)
 CTIS_FWD2(4, 4, 14)
 CTIS_FWD2(4, 4, 16)
 
-#define CTIS_BACK4(NB)                                                                                     \
+#define CTIS_BACK4(NB, POS, NAME)                                                                          \
   extern "C" __global__ void __launch_bounds__(kBack4Threads, 2)                                           \
-      ctis_back4_b##NB##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                      \
+      NAME(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                                      \
     if (A.frames == 0) return;                                                                             \
-    pdl_enter();                                                                                           \
     if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                             \
-    back_persistent4<NB>(A, &tm);                                                                          \
+    back_persistent4<NB, POS>(A, &tm);                                                                     \
   }
-CTIS_BACK4(2)
-CTIS_BACK4(4)
-CTIS_BACK4(8)
-CTIS_BACK4(12)
-CTIS_BACK4(16)
+CTIS_BACK4(2, 4, ctis_back4_b2_t)
+CTIS_BACK4(4, 4, ctis_back4_b4_t)
+CTIS_BACK4(8, 4, ctis_back4_b8_t)
+CTIS_BACK4(12, 4, ctis_back4_b12_t)
+CTIS_BACK4(16, 4, ctis_back4_b16_t)
+CTIS_BACK4(2, 2, ctis_back2_b2_t)
+CTIS_BACK4(4, 2, ctis_back2_b4_t)
+CTIS_BACK4(8, 2, ctis_back2_b8_t)
+CTIS_BACK4(12, 2, ctis_back2_b12_t)
+CTIS_BACK4(16, 2, ctis_back2_b16_t)
 
 #define CTIS_BACK(NB)                                                                                      \
   extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
