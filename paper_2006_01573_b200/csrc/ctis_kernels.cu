@@ -97,16 +97,26 @@ cudaError_t launch_validate(const float* x, long long count, int* flag, cudaStre
 // SMART log-ratio r_p = log(g_p / g_hat_p) where both are > 0, else 0 (R17); resets g_hat.
 __global__ void log_ratio_kernel(const float* __restrict__ g, float* gh, float* r, long long count) {
   pdl_enter();
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
-       i += (long long)gridDim.x * blockDim.x) {
-    const float gv = __ldg(g + i), hv = gh[i];
-    r[i] = (gv > 0.f && hv > 0.f) ? logf(__fdiv_rn(gv, hv)) : 0.f;
+  auto one = [](float gv, float hv) { return (gv > 0.f && hv > 0.f) ? logf(__fdiv_rn(gv, hv)) : 0.f; };
+  const bool aligned = ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(gh) |
+                         reinterpret_cast<uintptr_t>(r)) & 15u) == 0;
+  const long long n4 = aligned ? (count >> 2) : 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (long long i = t0; i < n4; i += stride) {
+    const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + i);
+    const float4 hv = reinterpret_cast<const float4*>(gh)[i];
+    reinterpret_cast<float4*>(r)[i] = make_float4(one(gv.x, hv.x), one(gv.y, hv.y), one(gv.z, hv.z), one(gv.w, hv.w));
+    reinterpret_cast<float4*>(gh)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (long long i = 4 * n4 + t0; i < count; i += stride) {
+    r[i] = one(__ldg(g + i), gh[i]);
     gh[i] = 0.f;
   }
 }
 
 cudaError_t launch_log_ratio(const float* g, float* ghat, float* r, long long count, cudaStream_t s, bool pdl) {
-  const long long want = (count + 255) / 256;
+  const long long want = (count / 4 + 255) / 256;
   const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
   return launch_ex(log_ratio_kernel, blocks, 256, s, pdl, g, ghat, r, count);
 }
@@ -117,16 +127,29 @@ cudaError_t launch_log_ratio(const float* g, float* ghat, float* r, long long co
 __global__ void ratio_ll_kernel(const float* __restrict__ g, float* gh, float* r, long long count, double* ll,
                                 const int* __restrict__ counter) {
   pdl_enter();
-  const long long stride = (long long)gridDim.x * blockDim.x;
   double acc = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += stride) {
-    const float gv = __ldg(g + i), hv = gh[i];
-    r[i] = hv > 0.f ? __fdiv_rn(gv, hv) : 0.f;
-    gh[i] = 0.f;
+  auto one = [&acc](float gv, float hv) -> float {
     if (hv > 0.f)
       acc += (double)gv * (double)logf(hv) - (double)hv;
     else if (gv > 0.f)
       acc = -INFINITY;
+    return hv > 0.f ? __fdiv_rn(gv, hv) : 0.f;
+  };
+  const bool aligned = ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(gh) |
+                         reinterpret_cast<uintptr_t>(r)) & 15u) == 0;
+  const long long n4 = aligned ? (count >> 2) : 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (long long i = t0; i < n4; i += stride) {
+    const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + i);
+    const float4 hv = reinterpret_cast<const float4*>(gh)[i];
+    const float rx = one(gv.x, hv.x), ry = one(gv.y, hv.y), rz = one(gv.z, hv.z), rw = one(gv.w, hv.w);
+    reinterpret_cast<float4*>(r)[i] = make_float4(rx, ry, rz, rw);
+    reinterpret_cast<float4*>(gh)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (long long i = 4 * n4 + t0; i < count; i += stride) {
+    r[i] = one(__ldg(g + i), gh[i]);
+    gh[i] = 0.f;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -144,7 +167,7 @@ __global__ void ratio_ll_kernel(const float* __restrict__ g, float* gh, float* r
 
 cudaError_t launch_ratio_ll(const float* g, float* ghat, float* r, long long count, double* ll, const int* counter,
                             cudaStream_t s, bool pdl) {
-  const long long want = (count + 255) / 256;
+  const long long want = (count / 4 + 255) / 256;
   const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
   return launch_ex(ratio_ll_kernel, blocks, 256, s, pdl, g, ghat, r, count, ll, counter);
 }
