@@ -429,3 +429,22 @@ def test_batched_frames_many_items_per_cta(ctis, dev):
         fi = torch.ones(geom.m, device=dev)
         plan.mlem(g[i].contiguous(), fi, 5)
         assert rel(fi.cpu().numpy(), fb[i].cpu().numpy()) <= 1e-6
+
+
+def test_C5_launch_configuration_sampled(ctis, oracle_lib, dev):
+    """C5 as bench.py runs it on one GPU: 256 C3 frames in one batched MLEM.  Sampled outputs: frames
+    0 and 255 equal their single-frame runs, frame 17 matches the oracle."""
+    cfg = syn.config("C5")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    F, K = cfg.frames, 3
+    scenes = torch.from_numpy(np.stack([syn.frame_scene(geom, i).reshape(-1) for i in range(F)])).to(dev)
+    g = plan.forward(scenes.view(F, geom.m))
+    fb = torch.ones(F, geom.m, device=dev)
+    plan.mlem(g, fb, K)
+    for i in (0, F - 1):
+        fi = torch.ones(geom.m, device=dev)
+        plan.mlem(g[i].contiguous(), fi, K)
+        assert rel(fi.cpu().numpy(), fb[i].cpu().numpy()) <= 1e-6
+    g17 = g[17].cpu().numpy()
+    assert rel(fb[17].cpu().numpy(), oracle_lib.mlem(geom, taps, g17, np.ones(geom.m), K)) <= 1e-5
