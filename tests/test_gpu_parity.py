@@ -448,3 +448,36 @@ def test_C5_launch_configuration_sampled(ctis, oracle_lib, dev):
         assert rel(fi.cpu().numpy(), fb[i].cpu().numpy()) <= 1e-6
     g17 = g[17].cpu().numpy()
     assert rel(fb[17].cpu().numpy(), oracle_lib.mlem(geom, taps, g17, np.ones(geom.m), K)) <= 1e-5
+
+
+def test_error_codes_new_entry_points(ctis, dev):
+    """ctis_mlem_monitored / ctis_smart / CTIS_OPT_PROJECTOR argument checking."""
+    import ctypes
+    from paper_2006_01573_b200 import _lib
+    geom = syn.Geometry(8, 8, 2, 32, 32)
+    plan = ctis.Plan.from_geometry(geom, syn.random_taps(geom, 3, seed=1))
+    g = torch.ones(geom.n, device=dev)
+    f = torch.ones(geom.m, device=dev)
+    ws = plan.workspace(1)
+    ll = torch.zeros(8, dtype=torch.float64, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int32, device=dev)
+    P = ctypes.c_void_p
+    call = lambda it, llp, cp: _lib.ctis_mlem_monitored(plan._h, P(g.data_ptr()), P(f.data_ptr()), it, 1e-3,
+                                                        P(ws.data_ptr()), llp, cp, P(0))
+    assert call(-1, P(ll.data_ptr()), P(cnt.data_ptr())) == ctis.ERR_INVALID_ARGUMENT
+    assert call(4, P(0), P(cnt.data_ptr())) == ctis.ERR_INVALID_ARGUMENT
+    assert call(4, P(ll.data_ptr() + 4), P(cnt.data_ptr())) == ctis.ERR_INVALID_ARGUMENT   # misaligned
+    assert call(4, P(ll.data_ptr()), P(cnt.data_ptr() + 2)) == ctis.ERR_INVALID_ARGUMENT
+    assert call(4, P(ll.data_ptr()), P(cnt.data_ptr())) == ctis.OK
+    torch.cuda.synchronize()
+    assert 2 <= int(cnt[0].item()) <= 4
+    with pytest.raises(ctis.CtisError) as ei:
+        plan.smart(g, f, -1)
+    assert ei.value.status == ctis.ERR_INVALID_ARGUMENT
+    with pytest.raises(ctis.CtisError) as ei:
+        plan.set_option(ctis.OPT_PROJECTOR, 2)
+    assert ei.value.status == ctis.ERR_INVALID_ARGUMENT
+    g[3] = -1.0
+    with pytest.raises(ctis.CtisError) as ei:
+        plan.smart(g, f, 2)
+    assert ei.value.status == ctis.ERR_DATA
