@@ -437,15 +437,6 @@ bool constant_bank_section(const unsigned char* img, size_t len, size_t& off, si
 // driver itself initialises the bank at module load (lazy or eager).  Writing the bank afterwards
 // with cudaMemcpy was not reliably seen by the first launches of a fresh plan (stale constant data
 // under lazy module loading: tests/test_gpu_parity.py::test_mlem_random_wrapping flaked after a C4 run).
-// TMA back kernel with four voxels per thread (256 threads); CTIS_BACK4=0 selects the 512-thread one
-bool back4_enabled() {
-  static bool v = [] {
-    const char* e = std::getenv("CTIS_BACK4");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return v;
-}
-
 ctis_status load_page(Page& pg, bool vec) {
   const size_t bytes = (size_t)(ctis_tables_cubin_end - ctis_tables_cubin);
   size_t off = 0, size = 0;
@@ -464,7 +455,7 @@ ctis_status load_page(Page& pg, bool vec) {
     name = "ctis_fwd_g" + std::to_string(pg.max_modes / 1000) + "_m" + std::to_string(pg.max_modes % 1000) +
            (vec ? "_t" : "_s");
   } else {
-    name = std::string(vec && back4_enabled() ? (pg.back_tc == 16 ? "ctis_back2_b" : "ctis_back4_b") : "ctis_back_b") +
+    name = std::string(vec ? (pg.back_tc == 16 ? "ctis_back2_b" : "ctis_back4_b") : "ctis_back_b") +
            std::to_string(pg.max_modes) + (vec ? "_t" : "_s");
   }
   CTIS_CUDA(cudaLibraryGetKernel(&pg.kern, pg.lib, name.c_str()), "cudaLibraryGetKernel");
@@ -552,39 +543,25 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     // 512-thread CTAs per SM, one per pass (G = 1, default: a CTA's prologue, first-window latency
     // and flush overlap the other CTA's tap loop; measured 78 vs 95 us at C4), or as one 1024-thread
     // CTA with two mode groups sharing each window (G = 2; CTIS_FWD_GROUPS=2).
-    // Default (TMA plans): forward_persistent2 — two u positions per thread, passes of <= 32 modes
-    // (CTIS_FWD_MAXM overrides the cap; templates: even MAXM <= 32, 36, 40).  CTIS_FWD_POS=1 selects
-    // the one-position kernel (forward_persistent / forward_body; also used by element-loader plans).
-    const char* pos_env = std::getenv("CTIS_FWD_POS");
-    const bool two_pos = P.tma_f && !(pos_env && std::atoi(pos_env) == 1);
+    // TMA plans: forward_persistent2 (two u positions per thread, 2 CTAs of 256 threads per SM), passes
+    // of <= 32 modes (CTIS_FWD_MAXM overrides the cap; templates: even MAXM <= 32, 36, 40).
+    // Element-loader plans: forward_body, 512 threads, up to 96 modes per pass.
     int maxm;
-    if (two_pos) {
+    if (P.tma_f) {
       const char* cap_env = std::getenv("CTIS_FWD_MAXM");
       const int cap = cap_env ? std::max(2, std::min(40, std::atoi(cap_env))) : 32;
       const int npass = (nm_max + cap - 1) / cap;
       int mm = std::max(2, ((nm_max + npass - 1) / npass + 1) / 2 * 2);
       if (mm > 32) mm = mm <= 36 ? 36 : 40;
-      // CTAs per SM (256 threads each): 2 (8-stage ring, <= 128 registers), 3 (6 stages, MAXM <= 24),
-      // 4 (4 stages, MAXM <= 16)
-      const char* occ_env = std::getenv("CTIS_FWD_OCC");
-      int occ = occ_env ? std::atoi(occ_env) : 2;
-      if (occ == 4 && mm > 16) occ = 3;
-      if (occ == 3 && mm > 24) occ = 2;
-      if (occ < 2 || occ > 4) occ = 2;
-      P.fwd_g = occ;
-
+      P.fwd_g = 2;
       P.fwd_m = mm;
       maxm = mm;
     } else {
-      if (nm_max <= 64) {
-        P.fwd_g = 1;
-        P.fwd_m = std::max(2, ((nm_max + 1) / 2 + 1) / 2 * 2);
-      } else {
-        P.fwd_g = 1;
-        P.fwd_m = std::max(40, std::min(96, (nm_max + 7) / 8 * 8));
-      }
-      // modes per pass (G = 1 with a small MAXM: two passes of MAXM modes)
-      maxm = (P.fwd_g == 1 && P.fwd_m <= 32) ? P.fwd_m : P.fwd_g * P.fwd_m;
+      P.fwd_g = 1;
+      P.fwd_m = nm_max <= 64 ? std::max(2, ((nm_max + 1) / 2 + 1) / 2 * 2)
+                             : std::max(40, std::min(96, (nm_max + 7) / 8 * 8));
+      // modes per pass: <= 64 modes run as two passes of MAXM (two independent CTAs per SM)
+      maxm = P.fwd_m;
     }
     std::vector<std::vector<const Mode*>> passes;
     std::vector<int> pass_chunk;
@@ -635,7 +612,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
       const char* e = std::getenv("CTIS_BACK_TC");
       // measured: tiny 14.8 -> 13.3 us, C2 unchanged, C3 (208 items) 25.0 -> 25.2 us: only below one item per SM
       const bool want16 = e ? std::atoi(e) == 16 : t32 * ((P.w + P.back_nb - 1) / P.back_nb) < (long long)P.sms;
-      if (want16 && P.tma_b && back4_enabled()) {
+      if (want16 && P.tma_b) {
         P.back_tc = 16;
         P.back_nb = choose_back_nb(P);
       }
@@ -950,15 +927,15 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
     cudaError_t e = make_tensor_map(&tm, fwd, P, src, frames);
     if (e != cudaSuccess) return e;
   }
-  const int threads = fwd ? (P.fwd_g >= 2 ? kFwd2Threads : kFwdThreads) : (tma && back4_enabled() ? kBack4Threads : kBackThreads);
-  const int stages = fwd ? (P.fwd_g == 3 ? 6 : P.fwd_g == 4 ? 4 : kFwdStages) : kBackStages;
+  const int threads = fwd ? (P.fwd_g == 2 ? kFwd2Threads : kFwdThreads) : (tma ? kBack4Threads : kBackThreads);
+  const int stages = fwd ? kFwdStages : kBackStages;
   const size_t smem = (size_t)stages * slot * sizeof(float) + 16 * stages;  // + full/empty mbarriers
   A.frames = frames;
   for (const Page& pg : pages) {
     // TMA kernels are persistent (2 CTAs per SM walk the page's items); element-loader kernels are
     // one CTA per (tile, chunk, frame)
     const long long items = (long long)pg.total_items * frames;
-    const int per_sm = fwd ? (P.fwd_g == 3 ? 3 : P.fwd_g == 4 ? 4 : 2) : 2;  // resident CTAs per SM
+    const int per_sm = 2;  // resident CTAs per SM (persistent TMA kernels)
     dim3 grid = tma ? dim3((unsigned)std::min<long long>(items, (long long)per_sm * P.sms), 1, 1)
                     : dim3(pg.max_tiles, pg.nchunks, frames);
     void* args[] = {&A, &tm};

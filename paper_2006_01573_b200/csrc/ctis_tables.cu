@@ -522,120 +522,6 @@ __device__ __forceinline__ void decode_item(int it, int per_frame, int nch, int&
   tile = r - tabi(kItemBase + lo);
 }
 
-template <int MAXM>
-__device__ __forceinline__ void forward_persistent(const TabArgs& A, const CUtensorMap* tm) {
-  extern __shared__ __align__(128) float smem[];
-  constexpr int S = kFwdStages, K = S / 2, MP = MAXM / 2;
-  const int nch = tabi(0);
-  const int per_frame = tabi(kItemBase + nch);
-  const int items = per_frame * A.frames;
-  if ((int)blockIdx.x >= items) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
-  const unsigned slot_bytes = 4u * A.slot_floats;
-  const unsigned full = sbase + S * slot_bytes;
-
-  // ---- producer state (thread 0): the next window of the stream
-  int p_item = blockIdx.x, p_band = 0, p_nb = 0, p_z = 0, p_Ur = 0, p_Uc = 0, p_lam0 = 0;
-  uint32_t p_BI = 0;
-  unsigned p_w = 0;
-  auto p_load_item = [&]() {
-    int k, tile;
-    decode_item(p_item, per_frame, nch, p_z, k, tile);
-    const uint32_t D = c_tab[1 + k];
-    const int tiles_r = tabi(D + 5), nm = tabi(D + 2);
-    p_lam0 = tabi(D + 0);
-    p_nb = tabi(D + 1);
-    p_Ur = tabi(D + 3) + (tile % tiles_r) * kFwdTR;
-    p_Uc = tabi(D + 4) + (tile / tiles_r) * kFwdTC;
-    p_BI = D + kDescHeader + ((nm + 3) & ~3);
-    p_band = 0;
-  };
-  auto issue_one = [&]() {
-    if (p_item >= items) return;
-    const unsigned slot = p_w & (S - 1);
-    const uint32_t bi = p_BI + 4 * p_band;
-    mbar_expect_tx(full + 8 * slot, A.box_bytes);
-    tma_4d(sbase + slot * slot_bytes, tm, p_Ur + tabi(bi + 0), p_Uc + tabi(bi + 1), p_lam0 + p_band, p_z,
-           full + 8 * slot);
-    ++p_w;
-    if (++p_band == p_nb) {
-      p_item += gridDim.x;
-      if (p_item < items) p_load_item();
-    }
-  };
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(full + 8 * s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    p_load_item();
-#pragma unroll
-    for (int s = 0; s < S; ++s) issue_one();
-  }
-  __syncthreads();
-
-  const unsigned tbase = sbase + 4u * (lane + A.box_r * warp);
-  const unsigned n = (unsigned)A.n;
-  unsigned w = 0, next_refill = K;
-  for (int it = blockIdx.x; it < items; it += gridDim.x) {
-    int z, k, tile;
-    decode_item(it, per_frame, nch, z, k, tile);
-    const uint32_t D = c_tab[1 + k];
-    const int nb = tabi(D + 1), nm = tabi(D + 2), tiles_r = tabi(D + 5);
-    const int U_r = tabi(D + 3) + (tile % tiles_r) * kFwdTR, U_c = tabi(D + 4) + (tile / tiles_r) * kFwdTC;
-    const uint32_t TP = D + kDescHeader + ((nm + 3) & ~3) + 4 * nb;
-    float2 acc[MP];
-#pragma unroll
-    for (int q = 0; q < MP; ++q) acc[q] = make_float2(0.f, 0.f);
-    auto compute = [&](unsigned base, int b) {
-      const uint4* ent = tab4(TP) + b * MP;
-#pragma unroll
-      for (int q = 0; q < MP; ++q) {
-        const uint4 e = ent[q];
-        const float2 x = make_float2(lds(base + e.x), lds(base + e.y));
-        acc[q] = __ffma2_rn(make_float2(__uint_as_float(e.z), __uint_as_float(e.w)), x, acc[q]);
-      }
-    };
-    for (int b = 0; b < nb;) {
-      if (w >= next_refill) {
-        __syncthreads();  // every warp has consumed the windows before w: their slots are free
-        if (threadIdx.x == 0) {
-#pragma unroll 1
-          for (int q = 0; q < S; ++q)  // catch up fully: refill points can land one window late
-            if (p_w < w + S) issue_one();
-        }
-        next_refill = w + K;
-      }
-      const unsigned s0 = w & (S - 1);
-      mbar_wait(full + 8 * s0, (w / S) & 1u);
-      compute(tbase + s0 * slot_bytes, b);
-      if (b + 1 < nb) {
-        const unsigned s1 = (w + 1) & (S - 1);
-        mbar_wait(full + 8 * s1, ((w + 1) / S) & 1u);
-        compute(tbase + s1 * slot_bytes, b + 1);
-        w += 2;
-        b += 2;
-      } else {
-        w += 1;
-        b += 1;
-      }
-    }
-    // flush this item: g_hat[(E(u) + o_ref) mod n] += acc (see forward_group)
-    float* g = A.dst + (long long)z * A.dst_frame;
-    unsigned ub = (unsigned)((U_r + lane) + A.gamma * (U_c + warp)) + A.bias;
-    for (int q = 0; q < A.nsub; ++q) ub = min(ub, ub - n);
-#pragma unroll
-    for (int c = 0; c < MAXM; ++c) {
-      const float v = (c & 1) ? acc[c >> 1].y : acc[c >> 1].x;
-      if (c < nm && v != 0.f) {
-        unsigned P = ub + c_tab[D + kDescHeader + c];
-        P = min(P, P - n);
-        atomicAdd(g + P, v);
-      }
-    }
-  }
-}
-
-
 // Forward, two u positions per thread (columns warp and warp + 8 of a 32 x 16 tile; 256 threads):
 // every tap entry read through the uniform datapath (LDCU.64) feeds four shared-memory loads and two
 // FFMA2, halving the table and loop-control instructions per tap of forward_persistent (the kernel
@@ -774,138 +660,6 @@ __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUte
         P1 = min(P1, P1 - n);
         red_nz(g + P0, (c & 1) ? a0[c >> 1].y : a0[c >> 1].x);
         red_nz(g + P1, (c & 1) ? a1[c >> 1].y : a1[c >> 1].x);
-      }
-    }
-  }
-}
-
-template <int NB>
-__device__ __forceinline__ void back_persistent(const TabArgs& A, const CUtensorMap* tm) {
-  extern __shared__ __align__(128) float smem[];
-  constexpr int S = kBackStages, K = S / 2, BP = NB / 2;
-  constexpr int NWARPS = kBackThreads / 32;
-  const int nch = tabi(0);
-  const int per_frame = tabi(kItemBase + nch);
-  const int items = per_frame * A.frames;
-  if ((int)blockIdx.x >= items) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
-  const unsigned slot_bytes = 4u * A.slot_floats;
-  const unsigned full = sbase + S * slot_bytes;
-
-  // window origin of mode c of the tile at (q_r0, q_c0): host-split Bm = Bm_r + gamma*Bm_c, one carry
-  // and one wrap (the plan only selects this kernel when no window of the page wraps)
-  auto origin_rc = [&](uint32_t MI, int c, int q_r0, int q_c0, int& R0, int& C0) {
-    R0 = q_r0 + tabi(MI + 4 * c + 0);
-    C0 = q_c0 + tabi(MI + 4 * c + 1);
-    if (R0 >= A.gamma) {
-      R0 -= A.gamma;
-      C0 += 1;
-    }
-    if (C0 >= A.xi) C0 -= A.xi;
-  };
-  int p_item = blockIdx.x, p_mode = 0, p_nm = 0, p_z = 0, p_qr = 0, p_qc = 0;
-  uint32_t p_MI = 0;
-  unsigned p_w = 0;
-  auto p_load_item = [&]() {
-    int k, tile;
-    decode_item(p_item, per_frame, nch, p_z, k, tile);
-    const uint32_t D = c_tab[1 + k];
-    const int tiles_r = tabi(D + 3);
-    p_nm = tabi(D + 2);
-    p_qr = (tile % tiles_r) * kBackTR;
-    p_qc = (tile / tiles_r) * kBackTC;
-    p_MI = D + kDescHeader;
-    p_mode = 0;
-  };
-  auto issue_one = [&]() {
-    if (p_item >= items) return;
-    const unsigned slot = p_w & (S - 1);
-    int R0, C0;
-    origin_rc(p_MI, p_mode, p_qr, p_qc, R0, C0);
-    mbar_expect_tx(full + 8 * slot, A.box_bytes);
-    tma_3d(sbase + slot * slot_bytes, tm, R0, C0, p_z, full + 8 * slot);
-    ++p_w;
-    if (++p_mode == p_nm) {
-      p_item += gridDim.x;
-      if (p_item < items) p_load_item();
-    }
-  };
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < S; ++q) mbar_init(full + 8 * q, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    p_load_item();
-#pragma unroll
-    for (int q = 0; q < S; ++q) issue_one();
-  }
-  __syncthreads();
-
-  const unsigned t0 = sbase + 4u * (lane + A.box_r * warp), t1 = t0 + 4u * A.box_r * NWARPS;
-  unsigned w = 0, next_refill = K;
-  for (int it = blockIdx.x; it < items; it += gridDim.x) {
-    int z, k, tile;
-    decode_item(it, per_frame, nch, z, k, tile);
-    const uint32_t D = c_tab[1 + k];
-    const int lam0 = tabi(D + 0), nb = tabi(D + 1), nm = tabi(D + 2), tiles_r = tabi(D + 3);
-    const int q_r0 = (tile % tiles_r) * kBackTR, q_c0 = (tile / tiles_r) * kBackTC;
-    const uint32_t MI = D + kDescHeader, TP = MI + 4 * nm, IH = TP + 2 * nm * NB;
-    float2 acc0[BP], acc1[BP];
-#pragma unroll
-    for (int q = 0; q < BP; ++q) acc0[q] = acc1[q] = make_float2(0.f, 0.f);
-    auto compute = [&](unsigned b0a, unsigned b1a, int c) {
-      const uint4* ent = tab4(TP) + c * BP;
-#pragma unroll
-      for (int q = 0; q < BP; ++q) {
-        const uint4 e = ent[q];
-        const float2 wv = make_float2(__uint_as_float(e.z), __uint_as_float(e.w));
-        acc0[q] = __ffma2_rn(wv, make_float2(lds(b0a + e.x), lds(b0a + e.y)), acc0[q]);
-        acc1[q] = __ffma2_rn(wv, make_float2(lds(b1a + e.x), lds(b1a + e.y)), acc1[q]);
-      }
-    };
-    for (int c = 0; c < nm;) {
-      if (w >= next_refill) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-#pragma unroll 1
-          for (int q = 0; q < S; ++q)  // catch up fully: refill points can land one window late
-            if (p_w < w + S) issue_one();
-        }
-        next_refill = w + K;
-      }
-      const unsigned s0 = w & (S - 1);
-      mbar_wait(full + 8 * s0, (w / S) & 1u);
-      compute(t0 + s0 * slot_bytes, t1 + s0 * slot_bytes, c);
-      if (c + 1 < nm) {
-        const unsigned s1 = (w + 1) & (S - 1);
-        mbar_wait(full + 8 * s1, ((w + 1) / S) & 1u);
-        compute(t0 + s1 * slot_bytes, t1 + s1 * slot_bytes, c + 1);
-        w += 2;
-        c += 2;
-      } else {
-        w += 1;
-        c += 1;
-      }
-    }
-    // epilogue of this item: f <- f * z * (1/h_lam) (or z)
-    float* f = A.dst + (long long)z * A.dst_frame;
-    const int qr = q_r0 + lane, qc0 = q_c0 + warp, qc1 = qc0 + NWARPS;
-    if (qr < A.a) {
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        if (b < nb) {
-          const long long lb = (long long)(lam0 + b) * A.ell + qr;
-          const float ih = tabf(IH + b);
-          const float z0 = (b & 1) ? acc0[b >> 1].y : acc0[b >> 1].x;
-          const float z1 = (b & 1) ? acc1[b >> 1].y : acc1[b >> 1].x;
-          if (qc0 < A.alpha) {
-            float* p = f + lb + (long long)A.a * qc0;
-            *p = upd_value(A.mode, *p, z0, ih);
-          }
-          if (qc1 < A.alpha) {
-            float* p = f + lb + (long long)A.a * qc1;
-            *p = upd_value(A.mode, *p, z1, ih);
-          }
-        }
       }
     }
   }
@@ -1087,19 +841,13 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
 
 }  // namespace
 
+// Element-loader forward (plans whose geometry rules out TMA boxes: a % 4 != 0)
 #define CTIS_FWD(M, MINB)                                                                                  \
-  extern "C" __global__ void __launch_bounds__(kFwdThreads, MINB)                                          \
-      ctis_fwd_g1_m##M##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                      \
-    if (A.frames == 0) return;                                                                             \
-    pdl_enter();                                                                                           \
-    if (A.dbg & 8) nan_fill_smem(kFwdStages * A.slot_floats);                                                  \
-    forward_persistent<M>(A, &tm);                                                                         \
-  }                                                                                                        \
   extern "C" __global__ void __launch_bounds__(kFwdThreads, MINB)                                          \
       ctis_fwd_g1_m##M##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                      \
     if (A.frames == 0) return;                                                                             \
     pdl_enter();                                                                                           \
-    if (A.dbg & 8) nan_fill_smem(kFwdStages * A.slot_floats);                                                  \
+    if (A.dbg & 8) nan_fill_smem(kFwdStages * A.slot_floats);                                             \
     forward_body<1, M, false, true>(A, &tm);                                                               \
   }
 CTIS_FWD(2, 2)
@@ -1153,26 +901,6 @@ CTIS_FWD2(2, 8, 30)
 CTIS_FWD2(2, 8, 32)
 CTIS_FWD2(2, 8, 36)
 CTIS_FWD2(2, 8, 40)
-CTIS_FWD2(3, 6, 2)
-CTIS_FWD2(3, 6, 4)
-CTIS_FWD2(3, 6, 6)
-CTIS_FWD2(3, 6, 8)
-CTIS_FWD2(3, 6, 10)
-CTIS_FWD2(3, 6, 12)
-CTIS_FWD2(3, 6, 14)
-CTIS_FWD2(3, 6, 16)
-CTIS_FWD2(3, 6, 18)
-CTIS_FWD2(3, 6, 20)
-CTIS_FWD2(3, 6, 22)
-CTIS_FWD2(3, 6, 24)
-CTIS_FWD2(4, 4, 2)
-CTIS_FWD2(4, 4, 4)
-CTIS_FWD2(4, 4, 6)
-CTIS_FWD2(4, 4, 8)
-CTIS_FWD2(4, 4, 10)
-CTIS_FWD2(4, 4, 12)
-CTIS_FWD2(4, 4, 14)
-CTIS_FWD2(4, 4, 16)
 
 #define CTIS_BACK4(NB, POS, NAME)                                                                          \
   extern "C" __global__ void __launch_bounds__(kBack4Threads, 2)                                           \
@@ -1192,19 +920,13 @@ CTIS_BACK4(8, 2, ctis_back2_b8_t)
 CTIS_BACK4(12, 2, ctis_back2_b12_t)
 CTIS_BACK4(16, 2, ctis_back2_b16_t)
 
+// Element-loader back projection (wrapped r windows or gamma % 4 != 0)
 #define CTIS_BACK(NB)                                                                                      \
-  extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
-      ctis_back_b##NB##_t(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                       \
-    if (A.frames == 0) return;                                                                             \
-    pdl_enter();                                                                                           \
-    if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                                 \
-    back_persistent<NB>(A, &tm);                                                                     \
-  }                                                                                                        \
   extern "C" __global__ void __launch_bounds__(kBackThreads, 2)                                            \
       ctis_back_b##NB##_s(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                       \
     if (A.frames == 0) return;                                                                             \
     pdl_enter();                                                                                           \
-    if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                                 \
+    if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                             \
     back_body<NB, false, true>(A, &tm);                                                                    \
   }
 CTIS_BACK(2)
