@@ -620,7 +620,8 @@ __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUte
 #pragma unroll 1
     for (int b = 0; b < nb; ++b, ++w) {
       if (w >= next_refill) {
-        __syncthreads();  // every warp has consumed the windows before w: their slots are free
+        if (!(A.dbg & 16)) __syncthreads();  // every warp has consumed the windows before w: slots free
+        // (CTIS_DEBUG & 16: profiling only — no refill barrier, results invalid; measures its cost)
         if (threadIdx.x == 0 && !(A.dbg & 1)) {
 #pragma unroll 1
           for (int q = 0; q < S; ++q)  // catch up fully: refill points can land one window late
