@@ -113,6 +113,7 @@ struct ctis_plan_s {
   int fwd_g = 1, fwd_m = 8;
   int sms = 148;
   bool pair = false;  // FFMA2 on tap pairs (16-byte entries) or plain FFMA (8-byte entries)
+  bool nowrap = false;  // no tap carries across FPA columns or wraps past n (2-D translations only)
   std::vector<Page> fwd, back;
   float* d_hband = nullptr;
   int* d_flag = nullptr;
@@ -508,6 +509,10 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
   // TMA needs 16-byte global strides: a % 4 == 0 for f, gamma % 4 == 0 for r.
   P.pair = true;  // FFMA2 on tap pairs (plain FFMA measured no faster on B200)
   P.tma_f = (P.a % 4 == 0);
+  P.nowrap = true;
+  for (const auto& b : bands)
+    for (const TapXY& t : b)
+      if (t.dr > P.gamma - P.a || t.dc > P.xi - P.alpha) P.nowrap = false;
   P.tma_b = (P.gamma % 4 == 0);
   // ---- forward: chunks of <= kFwdBands bands, modes split into passes of <= 96; one kernel template
   //      (G groups x MAXM modes, MAXM even: modes are paired for FFMA2) and one TMA box per plan
@@ -920,7 +925,7 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
   const int cap = fwd ? kFwdWinFloats : kBackWinFloats;
   int slot = tma ? (box_r * box_c + 31) / 32 * 32 : cap;
   TabArgs A{src, dst, src_frame, dst_frame, P.a, P.alpha, P.gamma, P.xi, P.n, P.ell, mode, bias, nsub,
-            slot, box_r, box_c, (unsigned)(4 * box_r * box_c), debug_flags(), frames};
+            slot, box_r, box_c, (unsigned)(4 * box_r * box_c), debug_flags(), frames, P.nowrap ? 1 : 0};
   alignas(64) CUtensorMap tm;
   std::memset(&tm, 0, sizeof(tm));
   if (tma) {

@@ -78,6 +78,7 @@ struct TabArgs {
   unsigned box_bytes;  // 4 * box_r * box_c
   int dbg;             // profiling switches (CTIS_DEBUG env): 1 = no TMA (compute on stale windows), 2 = no flush
   int frames;          // persistent kernels: frames in the launch (items = frames x page items)
+  int nowrap;          // every tap is a plain 2-D translation inside the FPA (no carry / wrap of Eq. 7)
 };
 
 }  // namespace ctis

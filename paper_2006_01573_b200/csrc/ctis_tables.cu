@@ -648,6 +648,23 @@ __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUte
       if (t == -1.f) g[0] = t;
       continue;
     }
+    if (A.nowrap) {
+      // no tap wraps: every nonzero accumulator's pixel E(u) + o_ref is the exact FPA index in [0, n)
+      // (E(q) + o of each contributing tap), so no modular reduction; zero accumulators (positions u
+      // outside every band's live range) are never stored, so their out-of-range addresses are unused
+      const float* gz = g;
+      const long long e0 = (long long)(U_r + lane) + (long long)A.gamma * (U_c + warp);
+      const long long e1 = e0 + (long long)A.gamma * NW;
+#pragma unroll
+      for (int c = 0; c < MAXM; ++c) {
+        if (c < nm) {
+          const unsigned o = c_tab[D + kDescHeader + c];
+          red_nz(const_cast<float*>(gz) + (e0 + o), (c & 1) ? a0[c >> 1].y : a0[c >> 1].x);
+          red_nz(const_cast<float*>(gz) + (e1 + o), (c & 1) ? a1[c >> 1].y : a1[c >> 1].x);
+        }
+      }
+      continue;
+    }
     unsigned ub0 = (unsigned)((U_r + lane) + A.gamma * (U_c + warp)) + A.bias;
     for (int q = 0; q < A.nsub; ++q) ub0 = min(ub0, ub0 - n);
     unsigned ub1 = ub0 + (unsigned)(((unsigned long long)A.gamma * NW) % n);  // E(u + NW columns) mod n
