@@ -35,7 +35,7 @@ $(PKG)/libctis.so: build/ctis_api.o build/ctis_kernels.o build/ctis_fft.o build/
 	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC -o $@.tmp $^ -lcufft && mv $@.tmp $@
 
 oracle/liboracle.so: oracle/ctis_oracle.c
-	gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -std=c99 -o $@ $<
+	gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -fPIC -shared -std=c99 -o $@ $<
 
 build/microbench: tools/microbench.cu
 	@mkdir -p build

@@ -28,7 +28,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
-CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c99"]
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=c99"]
 
 
 def build(force: bool = False) -> str:
@@ -65,6 +65,12 @@ def _load():
             lib.oracle_smart.argtypes = geo + [P, P, P, P, P, i64]
             lib.oracle_smart.restype = ctypes.c_int
             lib.oracle_mlem.restype = ctypes.c_int
+            for name in ("oracle_forward_par", "oracle_backproject_par"):
+                getattr(lib, name).argtypes = geo + [P, P, P, P, P, ctypes.c_int]
+                getattr(lib, name).restype = ctypes.c_int
+            lib.oracle_set_threads.argtypes = [ctypes.c_int]
+            lib.oracle_set_threads.restype = ctypes.c_int
+            lib.oracle_get_threads.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -87,6 +93,58 @@ def _taps(taps):
 def _check(rc: int, what: str):
     if rc != 0:
         raise ValueError(f"oracle {what} failed with code {rc}")
+
+
+def set_threads(nthreads: int) -> int:
+    """Threads for mlem / mlem_monitored / smart / sensitivity (OpenMP; 1 = the serial functions).
+
+    The parallel path performs the same floating-point operations per output element as the
+    serial one (bit-identical results; tests/test_oracle_pins.py::test_parallel_oracle_*)."""
+    return int(_load().oracle_set_threads(int(nthreads)))
+
+
+def get_threads() -> int:
+    return int(_load().oracle_get_threads())
+
+
+class threads:
+    """Context manager: `with oracle.threads(os.cpu_count()): oracle.mlem(...)`."""
+
+    def __init__(self, nthreads: int):
+        self.n = int(nthreads)
+
+    def __enter__(self):
+        self.prev = get_threads()
+        set_threads(self.n)
+        return self
+
+    def __exit__(self, *exc):
+        set_threads(self.prev)
+        return False
+
+
+def forward_par(geom, taps, f, nthreads: int) -> np.ndarray:
+    """g = H f with oracle_forward_par (bit-identical to forward(); distinct offsets per band)."""
+    lib = _load()
+    ptr, off, wt = _taps(taps)
+    fd = np.ascontiguousarray(np.asarray(f, np.float64).reshape(-1))
+    assert fd.size == geom.m
+    g = np.empty(geom.n, np.float64)
+    _check(lib.oracle_forward_par(*_geo(geom), _ptr(ptr), _ptr(off), _ptr(wt), _ptr(fd), _ptr(g), int(nthreads)),
+           "forward_par")
+    return g
+
+
+def backproject_par(geom, taps, u, nthreads: int) -> np.ndarray:
+    """zeta = H^T u with oracle_backproject_par (bit-identical to backproject())."""
+    lib = _load()
+    ptr, off, wt = _taps(taps)
+    ud = np.ascontiguousarray(np.asarray(u, np.float64).reshape(-1))
+    assert ud.size == geom.n
+    z = np.empty(geom.m, np.float64)
+    _check(lib.oracle_backproject_par(*_geo(geom), _ptr(ptr), _ptr(off), _ptr(wt), _ptr(ud), _ptr(z), int(nthreads)),
+           "backproject_par")
+    return z
 
 
 def embed_index(geom, j: int) -> int:

@@ -34,6 +34,15 @@
  *            offset and the walk starts at the first tap that wraps past n.
  * Build with -O2 -ffp-contract=off (no fused multiply-add, no fast-math).
  *
+ * Threads (oracle_set_threads, OpenMP): the paper-sized configurations (C4: 321 M tap incidences
+ * per projection) take seconds per iteration on one core.  With more than one thread, MLEM, SMART
+ * and the monitored MLEM run forward/back through oracle_forward_par / oracle_backproject_par and
+ * split their element-wise loops over threads.  Every output element still receives exactly the
+ * same sequence of floating-point operations as in the serial functions (the parallel forward walks
+ * each pixel's terms in ascending j, see oracle_forward_par), so the results are bit-identical to the
+ * serial path; tests/test_oracle_pins.py pins that.  The serial oracle_forward / oracle_backproject
+ * stay the functions checked against the dense H.
+ *
  * Pins (tests/test_oracle_*.py, all -m "not gpu"): dense H built literally from
  * Eqs. 3-7 (bit-exact), the paper's own FFT algorithm Eqs. 13/17 (<= 1e-12),
  * scipy convolve2d/correlate2d for non-wrapping taps, impulse/shift identities,
@@ -45,6 +54,9 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 /* Error codes of the oracle (small, independent of the product's). */
 #define OR_OK 0
@@ -147,6 +159,136 @@ int oracle_backproject(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
     return OR_OK;
 }
 
+/* ---- thread count for MLEM / SMART / monitored MLEM (1 = the plain serial functions) ---------- */
+static int g_threads = 1;
+
+int oracle_set_threads(int nthreads) {
+#ifdef _OPENMP
+    g_threads = nthreads < 1 ? 1 : nthreads;
+#else
+    (void)nthreads;
+    g_threads = 1;
+#endif
+    return g_threads;
+}
+
+int oracle_get_threads(void) { return g_threads; }
+
+static int check_distinct(int64_t w, const int64_t* ptr, const int64_t* off, const int64_t* order) {
+    for (int64_t s = 0; s < w; ++s)
+        for (int64_t q = ptr[s] + 1; q < ptr[s + 1]; ++q)
+            if (off[order[q]] == off[order[q - 1]]) return OR_ETAP;
+    return OR_OK;
+}
+
+/* g = H f, the same sums as oracle_forward, split over threads by ranges of output pixels p.
+ * oracle_forward adds the terms of g[p] in ascending voxel index j = s*l + (k's row + a*k's column),
+ * i.e. band s ascending, then ascending k = (p - o) mod n within the band.  Here each thread owns
+ * pixels [P0, P1) and, band by band, applies the band's taps so that every pixel sees them in that
+ * same order: for a fixed p, ascending k means first the taps with o <= p in descending o (k = p - o),
+ * then the taps with o > p in descending o (k = p - o + n > p).  The set {o <= p} only changes at
+ * p = o, so [P0, P1) is cut at every tap offset inside it; on each piece [q0, q1) one tap order holds
+ * for all its pixels, and each tap covers the contiguous k range [q0 - o, q1 - o) (mod n), walked over
+ * the columns of the field-stop image E (Eq. 11) it meets.  Offsets must be distinct within a band
+ * (OR_ETAP otherwise; the serial function accepts duplicates). */
+int oracle_forward_par(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi,
+                       const int64_t* tap_ptr, const int64_t* tap_offset, const double* tap_weight,
+                       const double* f, double* g, int nthreads) {
+    int rc = check_geom(a, alpha, w, gamma, xi);
+    if (rc) return rc;
+    int64_t n = gamma * xi, l = a * alpha;
+    if ((rc = check_taps(w, n, tap_ptr, tap_offset))) return rc;
+    int64_t nnz = tap_ptr[w];
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nnz > 0 ? nnz : 1));
+    if (!order) return OR_ENOMEM;
+    for (int64_t s = 0; s < w; ++s) sort_band(tap_offset, tap_ptr[s], tap_ptr[s + 1], order + tap_ptr[s]);
+    if ((rc = check_distinct(w, tap_ptr, tap_offset, order))) { free(order); return rc; }
+    int64_t nchunks = (int64_t)(nthreads < 1 ? 1 : nthreads) * 16;
+    if (nchunks > n) nchunks = n;
+    #pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads < 1 ? 1 : nthreads)
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+        int64_t P0 = n * ch / nchunks, P1 = n * (ch + 1) / nchunks;
+        for (int64_t p = P0; p < P1; ++p) g[p] = 0.0;
+        for (int64_t s = 0; s < w; ++s) {
+            const int64_t* ord = order + tap_ptr[s];
+            int64_t cnt = tap_ptr[s + 1] - tap_ptr[s];
+            if (cnt == 0) continue;
+            int64_t c = 0;                                  /* taps with o <= q0 */
+            while (c < cnt && tap_offset[ord[c]] <= P0) ++c;
+            int64_t q0 = P0;
+            while (q0 < P1) {
+                int64_t q1 = (c < cnt && tap_offset[ord[c]] < P1) ? tap_offset[ord[c]] : P1;
+                for (int64_t q = 0; q < cnt; ++q) {          /* descending o, starting below q0 */
+                    int64_t t = ord[((c - 1 - q) % cnt + cnt) % cnt];
+                    int64_t o = tap_offset[t];
+                    int64_t k0 = o <= q0 ? q0 - o : q0 - o + n, k1 = k0 + (q1 - q0);
+                    for (int64_t col = k0 / gamma; col < alpha && col * gamma < k1; ++col) {
+                        int64_t r0 = k0 - col * gamma > 0 ? k0 - col * gamma : 0;
+                        int64_t r1 = k1 - col * gamma < a ? k1 - col * gamma : a;
+                        for (int64_t r = r0; r < r1; ++r) {
+                            int64_t k = col * gamma + r;
+                            int64_t p = (k + o) % n;
+                            int64_t j = s * l + r + a * col;
+                            double prod = tap_weight[t] * f[j];
+                            g[p] = g[p] + prod;
+                        }
+                    }
+                }
+                q0 = q1;
+                while (c < cnt && tap_offset[ord[c]] <= q0) ++c;
+            }
+        }
+    }
+    free(order);
+    return OR_OK;
+}
+
+/* zeta = H^T u, the same per-voxel sums as oracle_backproject (every zeta_i is independent), split
+ * over threads by voxel. */
+int oracle_backproject_par(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi,
+                           const int64_t* tap_ptr, const int64_t* tap_offset, const double* tap_weight,
+                           const double* u, double* zeta, int nthreads) {
+    int rc = check_geom(a, alpha, w, gamma, xi);
+    if (rc) return rc;
+    int64_t n = gamma * xi, m = a * alpha * w;
+    if ((rc = check_taps(w, n, tap_ptr, tap_offset))) return rc;
+    int64_t nnz = tap_ptr[w];
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nnz > 0 ? nnz : 1));
+    if (!order) return OR_ENOMEM;
+    for (int64_t s = 0; s < w; ++s) sort_band(tap_offset, tap_ptr[s], tap_ptr[s + 1], order + tap_ptr[s]);
+    #pragma omp parallel for schedule(static) num_threads(nthreads < 1 ? 1 : nthreads)
+    for (int64_t i = 0; i < m; ++i) {
+        int64_t jj = oracle_extract_index(a, alpha, w, gamma, xi, i);
+        int64_t s = jj / n, k = jj - s * n;
+        const int64_t* ord = order + tap_ptr[s];
+        int64_t cnt = tap_ptr[s + 1] - tap_ptr[s];
+        int64_t start = 0;
+        while (start < cnt && tap_offset[ord[start]] < n - k) ++start;
+        double acc = 0.0;
+        for (int64_t q = 0; q < cnt; ++q) {
+            int64_t t = ord[(start + q) % cnt];
+            int64_t p = (k + tap_offset[t]) % n;
+            double prod = tap_weight[t] * u[p];
+            acc = acc + prod;
+        }
+        zeta[i] = acc;
+    }
+    free(order);
+    return OR_OK;
+}
+
+/* forward / back as used by the iterations: serial functions unless oracle_set_threads(> 1) */
+static int fwd(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi, const int64_t* tp,
+               const int64_t* to, const double* tw, const double* f, double* g) {
+    return g_threads > 1 ? oracle_forward_par(a, alpha, w, gamma, xi, tp, to, tw, f, g, g_threads)
+                         : oracle_forward(a, alpha, w, gamma, xi, tp, to, tw, f, g);
+}
+static int back(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi, const int64_t* tp,
+                const int64_t* to, const double* tw, const double* u, double* z) {
+    return g_threads > 1 ? oracle_backproject_par(a, alpha, w, gamma, xi, tp, to, tw, u, z, g_threads)
+                         : oracle_backproject(a, alpha, w, gamma, xi, tp, to, tw, u, z);
+}
+
 /* h = H^T 1: column sums h_j = sum_i H_ij. */
 int oracle_sensitivity(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi,
                        const int64_t* tap_ptr, const int64_t* tap_offset, const double* tap_weight,
@@ -157,7 +299,7 @@ int oracle_sensitivity(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
     double* ones = (double*)malloc(sizeof(double) * (size_t)n);
     if (!ones) return OR_ENOMEM;
     for (int64_t p = 0; p < n; ++p) ones[p] = 1.0;
-    rc = oracle_backproject(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, ones, h);
+    rc = back(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, ones, h);
     free(ones);
     return rc;
 }
@@ -177,9 +319,11 @@ int oracle_mlem(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi,
     if (!h || !gk || !u || !zeta) { rc = OR_ENOMEM; goto done; }
     if ((rc = oracle_sensitivity(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, h))) goto done;
     for (int64_t k = 0; k < iters; ++k) {
-        if ((rc = oracle_forward(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, f, gk))) goto done;
+        if ((rc = fwd(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, f, gk))) goto done;
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t p = 0; p < n; ++p) u[p] = gk[p] > 0.0 ? g[p] / gk[p] : 0.0;
-        if ((rc = oracle_backproject(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, u, zeta))) goto done;
+        if ((rc = back(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, u, zeta))) goto done;
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t j = 0; j < m; ++j) f[j] = (f[j] * zeta[j]) / h[j];
         if (ghat_out) memcpy(ghat_out, gk, sizeof(double) * (size_t)n);
     }
@@ -220,10 +364,12 @@ int oracle_mlem_monitored(int64_t a, int64_t alpha, int64_t w, int64_t gamma, in
     if (!h || !gk || !u || !zeta) { rc = OR_ENOMEM; goto done; }
     if ((rc = oracle_sensitivity(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, h))) goto done;
     for (int64_t k = 1; k <= max_iters; ++k) {
-        if ((rc = oracle_forward(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, f, gk))) goto done;
+        if ((rc = fwd(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, f, gk))) goto done;
         ll[k - 1] = oracle_loglik(n, g, gk);
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t p = 0; p < n; ++p) u[p] = gk[p] > 0.0 ? g[p] / gk[p] : 0.0;
-        if ((rc = oracle_backproject(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, u, zeta))) goto done;
+        if ((rc = back(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, u, zeta))) goto done;
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t j = 0; j < m; ++j) f[j] = (f[j] * zeta[j]) / h[j];
         *iters_done = k;
         if (k >= 2 && ll[k - 1] - ll[k - 2] <= rel_tol * fabs(ll[k - 1])) break;
@@ -251,9 +397,11 @@ int oracle_smart(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi,
     if (!h || !gk || !u || !zeta) { rc = OR_ENOMEM; goto done; }
     if ((rc = oracle_sensitivity(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, h))) goto done;
     for (int64_t k = 0; k < iters; ++k) {
-        if ((rc = oracle_forward(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, f, gk))) goto done;
+        if ((rc = fwd(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, f, gk))) goto done;
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t p = 0; p < n; ++p) u[p] = (g[p] > 0.0 && gk[p] > 0.0) ? log(g[p] / gk[p]) : 0.0;
-        if ((rc = oracle_backproject(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, u, zeta))) goto done;
+        if ((rc = back(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, u, zeta))) goto done;
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t j = 0; j < m; ++j) f[j] = f[j] * exp(zeta[j] / h[j]);
     }
 done:

@@ -421,3 +421,54 @@ def test_smart_single_unit_tap_is_exact_in_one_step(oracle_lib):
     g = oracle_lib.forward(geom, taps, ft)
     f = oracle_lib.smart(geom, taps, g, np.ones(geom.m), 1)
     assert np.max(np.abs(f - ft.reshape(-1))) <= 1e-12
+
+
+# --------------------------------------------------------------------------- threaded oracle
+PAR_GEOMS = GEOMS + _random_geoms(12, seed=23, max_nw=40_000)
+
+
+@pytest.mark.parametrize("gi", range(len(PAR_GEOMS)))
+@pytest.mark.parametrize("nthreads", [1, 3, 8])
+def test_parallel_oracle_is_bitwise_serial(oracle_lib, gi, nthreads):
+    """oracle_forward_par / oracle_backproject_par perform, per output element, the same floating-point
+    operations in the same order as the serial oracle (which the dense-H test pins bit for bit), for
+    any thread count and with wrapping taps: the results must be identical, not merely close."""
+    g = PAR_GEOMS[gi]
+    taps = syn.random_taps(g, (1, min(9, g.n)), seed=300 + gi, region="any")
+    rng = np.random.default_rng(7 + gi)
+    f = rng.random(g.m)
+    u = rng.standard_normal(g.n)
+    assert np.array_equal(oracle_lib.forward_par(g, taps, f, nthreads), oracle_lib.forward(g, taps, f))
+    assert np.array_equal(oracle_lib.backproject_par(g, taps, u, nthreads), oracle_lib.backproject(g, taps, u))
+
+
+def test_parallel_oracle_paper_workload_and_iterations(oracle_lib):
+    """C2 (paper-shaped taps, 25 bands on 512^2): threaded projections and 3 threaded MLEM / SMART /
+    monitored-MLEM iterations equal the serial ones bit for bit."""
+    cfg = syn.config("C2")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    f = syn.scene_blobs(geom).reshape(-1).astype(np.float64)
+    gs = oracle_lib.forward(geom, taps, f)
+    assert np.array_equal(oracle_lib.forward_par(geom, taps, f, 8), gs)
+    u = np.random.default_rng(3).random(geom.n)
+    assert np.array_equal(oracle_lib.backproject_par(geom, taps, u, 8), oracle_lib.backproject(geom, taps, u))
+    f0 = np.ones(geom.m)
+    ser = oracle_lib.mlem(geom, taps, gs, f0, 3)
+    sm = oracle_lib.smart(geom, taps, gs, f0, 2)
+    mon = oracle_lib.mlem_monitored(geom, taps, gs, f0, 3, 0.0)
+    with oracle_lib.threads(8):
+        assert oracle_lib.get_threads() in (1, 8)
+        par = oracle_lib.mlem(geom, taps, gs, f0, 3)
+        smp = oracle_lib.smart(geom, taps, gs, f0, 2)
+        monp = oracle_lib.mlem_monitored(geom, taps, gs, f0, 3, 0.0)
+    assert oracle_lib.get_threads() == 1
+    assert np.array_equal(par, ser)
+    assert np.array_equal(smp, sm)
+    assert np.array_equal(monp[0], mon[0]) and np.array_equal(monp[1], mon[1]) and monp[2] == mon[2]
+
+
+def test_parallel_forward_rejects_duplicate_offsets(oracle_lib):
+    g = syn.Geometry(2, 2, 1, 4, 4)
+    taps = syn.Taps(np.array([0, 2]), np.array([3, 3]), np.array([0.5, 0.25], np.float32))
+    with pytest.raises(ValueError):
+        oracle_lib.forward_par(g, taps, np.ones(g.m), 2)
