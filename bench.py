@@ -272,7 +272,8 @@ def main():
     if rank == 0:
         reps = 20
         fk = fbufs[-1].view(-1)[:m_loc] if frames == 1 else fbufs[-1][0]
-        rk = ws.view(-1)[:geom.n]
+        half = (geom.n * frames + 3) // 4 * 4                 # workspace = [g_hat accumulator | r]
+        rk = ws.view(-1)[half:half + geom.n]
         scratch = torch.zeros(geom.n, dtype=torch.float32, device=dev)
         fu = fbufs[0].view(-1)[:m_loc]
         for name, fn in (("forward", lambda: plan.forward_accumulate(fk, scratch)),

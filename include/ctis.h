@@ -118,6 +118,13 @@ CTIS_API void ctis_plan_destroy(ctis_plan plan);
  * band_end, total taps stored.  Host-side, no device work. */
 CTIS_API ctis_status ctis_plan_dims(ctis_plan plan, int64_t out[10]);
 
+/* Plan layout (host-side, no device work; tests and profiling): out[0..9] = forward tap pages,
+ * back tap pages, forward chunk passes, back chunks, forward uses TMA (0/1), back uses TMA (0/1),
+ * back bands per chunk (NB), back tile columns, forward modes per pass (MAXM), forward work items
+ * per frame.  A page is one 64 KB __constant__ bank of tap tables (one kernel launch per page and
+ * projection).  CTIS_ERR_INVALID_ARGUMENT if plan or out is NULL. */
+CTIS_API ctis_status ctis_plan_info(ctis_plan plan, int64_t out[10]);
+
 CTIS_API ctis_status ctis_set_option(ctis_plan plan, int option, int64_t value);
 
 /* Bytes of caller-allocated device workspace needed by ctis_mlem* and

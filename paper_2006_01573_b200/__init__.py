@@ -33,6 +33,7 @@ _SIGS = {
     "ctis_plan_create_shard": ([_i64] * 5 + [_P, _P, _P, _i64, _i64, _int, _P], _int),
     "ctis_plan_destroy": ([_P], None),
     "ctis_plan_dims": ([_P, _P], _int),
+    "ctis_plan_info": ([_P, _P], _int),
     "ctis_set_option": ([_P, _int, _i64], _int),
     "ctis_workspace_bytes": ([_P, _i64], ctypes.c_size_t),
     "ctis_forward": ([_P, _P, _P, _P], _int),
@@ -149,6 +150,14 @@ class Plan:
     @property
     def handle(self):
         return self._h
+
+    def info(self) -> dict:
+        """Plan layout (ctis_plan_info): tap pages, chunks, kernel family choices."""
+        v = (ctypes.c_int64 * 10)()
+        _check(_lib.ctis_plan_info(self._h, v), "ctis_plan_info")
+        keys = ("fwd_pages", "back_pages", "fwd_chunks", "back_chunks", "tma_f", "tma_b", "back_nb", "back_tc",
+                "fwd_maxm", "fwd_items")
+        return dict(zip(keys, (int(x) for x in v)))
 
     def set_option(self, option: int, value: int):
         _check(_lib.ctis_set_option(self._h, int(option), int(value)), "ctis_set_option")

@@ -722,8 +722,12 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
   if (a < 1 || alpha < 1 || w < 1 || gamma < 1 || xi < 1)
     return fail(CTIS_ERR_DIMENSION, "a, alpha, w, gamma, xi must be >= 1");
   if (gamma < a || xi < alpha) return fail(CTIS_ERR_DIMENSION, "field stop must fit the FPA (gamma >= a, xi >= alpha)");
+  // every factor below 2^30 before any product is formed (no int64 overflow); then the products
+  if (a >= (int64_t(1) << 30) || alpha >= (int64_t(1) << 30) || w >= (int64_t(1) << 30) ||
+      gamma >= (int64_t(1) << 30) || xi >= (int64_t(1) << 30))
+    return fail(CTIS_ERR_DIMENSION, "n must be < 2^30 and m < 2^31");
   const int64_t n = gamma * xi, ell = a * alpha;
-  if (n >= (int64_t(1) << 30) || ell * w >= (int64_t(1) << 31))
+  if (n >= (int64_t(1) << 30) || ell >= (int64_t(1) << 30) || ell * w >= (int64_t(1) << 31))
     return fail(CTIS_ERR_DIMENSION, "n must be < 2^30 and m < 2^31");
   if (b0 < 0 || b1 > w || b0 >= b1) return fail(CTIS_ERR_DIMENSION, "band range must be a non-empty subrange of [0, w)");
   if (tap_ptr[0] != 0) return fail(CTIS_ERR_TAP, "tap_ptr[0] must be 0");
@@ -1182,6 +1186,20 @@ void ctis_plan_destroy(ctis_plan plan) { delete plan; }
 ctis_status ctis_plan_dims(ctis_plan p, int64_t out[10]) {
   if (!p || !out) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL argument");
   const int64_t v[10] = {p->a, p->alpha, p->w, p->gamma, p->xi, p->n, p->m, p->band_begin, p->band_end, p->total_taps};
+  std::memcpy(out, v, sizeof(v));
+  return CTIS_OK;
+}
+
+ctis_status ctis_plan_info(ctis_plan p, int64_t out[10]) {
+  if (!p || !out) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL argument");
+  int64_t fch = 0, bch = 0, fitems = 0;
+  for (const Page& pg : p->fwd) {
+    fch += pg.nchunks;
+    fitems += pg.total_items;
+  }
+  for (const Page& pg : p->back) bch += pg.nchunks;
+  const int64_t v[10] = {(int64_t)p->fwd.size(), (int64_t)p->back.size(), fch, bch, p->tma_f ? 1 : 0,
+                         p->tma_b ? 1 : 0, p->back_nb, p->back_tc, p->fwd_m, fitems};
   std::memcpy(out, v, sizeof(v));
   return CTIS_OK;
 }

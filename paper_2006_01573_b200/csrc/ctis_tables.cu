@@ -648,7 +648,7 @@ __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUte
       if (t == -1.f) g[0] = t;
       continue;
     }
-    if (A.nowrap) {
+    if (A.nowrap && !(A.dbg & 1)) {  // (CTIS_DEBUG & 1 computes on stale windows: keep the modular path)
       // no tap wraps: every nonzero accumulator's pixel E(u) + o_ref is the exact FPA index in [0, n)
       // (E(q) + o of each contributing tap), so no modular reduction; zero accumulators (positions u
       // outside every band's live range) are never stored, so their out-of-range addresses are unused
@@ -924,6 +924,7 @@ CTIS_FWD2(2, 8, 40)
   extern "C" __global__ void __launch_bounds__(kBack4Threads, 2)                                           \
       NAME(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                                      \
     if (A.frames == 0) return;                                                                             \
+    pdl_enter();                                                                                           \
     if (A.dbg & 8) nan_fill_smem(kBackStages * A.slot_floats);                                             \
     back_persistent4<NB, POS>(A, &tm);                                                                     \
   }

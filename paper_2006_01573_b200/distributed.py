@@ -57,10 +57,18 @@ def mlem_band_sharded(plan, g, f_local, iters: int, all_reduce: Callable, ghat=N
     """
     if ghat is None:
         ghat = g.new_empty(plan.n)
-    for _ in range(int(iters)):
-        plan.forward(f_local, out=ghat, stream=stream)        # partial H_shard f_shard
-        all_reduce(ghat)                                      # g_hat = sum over shards (Eq. 3)
-        plan.back_update_from_ghat(g, ghat, f_local, ws=ws, stream=stream)
+    import contextlib
+    # all_reduce (torch.distributed) is ordered against the CURRENT stream: run the whole iteration on
+    # `stream` so the collective sees the finished partial g_hat and back_update sees the reduced one
+    ctx = contextlib.nullcontext()
+    if stream is not None and getattr(g, "is_cuda", False):
+        import torch
+        ctx = torch.cuda.stream(stream)
+    with ctx:
+        for _ in range(int(iters)):
+            plan.forward(f_local, out=ghat, stream=stream)        # partial H_shard f_shard
+            all_reduce(ghat)                                      # g_hat = sum over shards (Eq. 3)
+            plan.back_update_from_ghat(g, ghat, f_local, ws=ws, stream=stream)
     return f_local
 
 

@@ -38,5 +38,26 @@ for gi, (geom, region) in enumerate(cases):
     e3 = rel(fd.cpu().numpy(), oracle.mlem(geom, taps, g, np.ones(geom.m), 10))
     print(gi, e1, e2, e3)
     worst = max(worst, e1 / 1e-5, e2 / 1e-5, e3 / 1e-3)
+if len(sys.argv) > 1 and sys.argv[1] == "solvers":
+    # C2 (TMA forward + persistent TMA back) and a wrapping case: MLEM / SMART / monitored MLEM
+    cfg = syn.config("C2")
+    for geom, taps, ft in [(cfg.geom, syn.paper_taps(cfg), syn.scene_blobs(cfg.geom)),
+                           (syn.Geometry(33, 17, 6, 70, 45), syn.random_taps(syn.Geometry(33, 17, 6, 70, 45), (2, 9),
+                                                                               seed=77, region="any"),
+                            syn.scene_random(syn.Geometry(33, 17, 6, 70, 45), seed=3, lo=0.1))]:
+        plan = ctis.Plan.from_geometry(geom, taps)
+        g = oracle.forward(geom, taps, ft).astype(np.float32)
+        gd = torch.from_numpy(g).cuda()
+        fd = torch.ones(geom.m, device="cuda")
+        plan.mlem(gd, fd, 30)
+        e4 = rel(fd.cpu().numpy(), oracle.mlem(geom, taps, g, np.ones(geom.m), 30))
+        fs = torch.ones(geom.m, device="cuda")
+        plan.smart(gd, fs, 10)
+        e5 = rel(fs.cpu().numpy(), oracle.smart(geom, taps, g, np.ones(geom.m), 10))
+        fm = torch.ones(geom.m, device="cuda")
+        plan.mlem_monitored(gd, fm, 15, 0.0)
+        e6 = rel(fm.cpu().numpy(), oracle.mlem(geom, taps, g, np.ones(geom.m), 15))
+        print("solvers", geom, e4, e5, e6)
+        worst = max(worst, e4 / 1e-3, e5 / 1e-3, e6 / 1e-3)
 print("WORST", worst)
 sys.exit(0 if worst <= 1.0 else 1)
