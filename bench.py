@@ -117,12 +117,56 @@ def algorithmic(cfg, taps):
     }
 
 
-def cpu_oracle_iterations(cfg, taps, g, iters):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_oracle_iterations(cfg, taps, g, iters, threads=1):
+    """Time `iters` MLEM iterations of the fp64 oracle as it stands (oracle/; OpenMP over `threads`)."""
     import oracle
     f0 = np.ones(cfg.geom.m)
-    t0 = time.perf_counter()
-    oracle.mlem(cfg.geom, taps, g, f0, iters)
-    return time.perf_counter() - t0
+    with oracle.threads(threads):
+        t0 = time.perf_counter()
+        oracle.mlem(cfg.geom, taps, g, f0, iters)
+        return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, taps, g, K, workload, budget_s=12.0):
+    """The oracle on the host's cores (rank 0, N = 1): a bounded sample of the benchmarked workload on
+    every core, the same on one core, and full-K reconstructions of the small configs (tiny, C2)."""
+    import oracle
+    cores = host_cores()
+    t1 = cpu_oracle_iterations(cfg, taps, g, 1, cores)              # probe (includes h = H^T 1)
+    iters = int(max(1, min(K, budget_s / max(t1, 1e-3))))
+    t = cpu_oracle_iterations(cfg, taps, g, iters, cores)
+    t_single = cpu_oracle_iterations(cfg, taps, g, 1, 1)
+    small = {}
+    for name in ("tiny", "C2"):
+        c = syn.config(name)
+        tp = syn.paper_taps(c)
+        gs = oracle.forward(c.geom, tp, syn.scene_blobs(c.geom)).astype(np.float32).astype(np.float64)
+        small[name] = {"K": c.K, "s_per_recon_1_thread": cpu_oracle_iterations(c, tp, gs, c.K, 1),
+                       f"s_per_recon_{cores}_threads": cpu_oracle_iterations(c, tp, gs, c.K, cores)}
+    return {"value": iters / t, "unit": "iterations/s", "cores": cores, "kind": "oracle",
+            "cpu": cpu_model(),
+            "sample": f"{workload}: {iters} MLEM iterations (of K={K}) on {cores} threads, {t:.1f} s; "
+                      f"recon/s = value/{K} (extrapolated from the sample)",
+            "single_thread": {"value": 1.0 / t_single, "unit": "iterations/s", "sample": f"{workload}: 1 iteration"},
+            "full_K_small_configs": small}
 
 
 def run_reference(args):
@@ -135,9 +179,10 @@ def run_reference(args):
     geom = cfg.geom
     taps = syn.paper_taps(cfg)
     g = oracle.forward(geom, taps, syn.scene_blobs(geom)).astype(np.float32).astype(np.float64)
+    cores = host_cores()
     for _ in range(max(0, min(args.warmup, 1))):
-        cpu_oracle_iterations(cfg, taps, g, 1)
-    times = [cpu_oracle_iterations(cfg, taps, g, 1) for _ in range(args.steps)]
+        cpu_oracle_iterations(cfg, taps, g, 1, cores)
+    times = [cpu_oracle_iterations(cfg, taps, g, 1, cores) for _ in range(args.steps)]
     total = sum(times)
     value = args.steps / total
     line = {
@@ -148,16 +193,31 @@ def run_reference(args):
                    "xi": geom.xi, "taps_per_band": int(taps.ptr[1]), "iterations_per_step": 1,
                    "recon_iterations": cfg.K, "l2": "inputs resident in host RAM; CPU run"},
         "recon_per_s": value / cfg.K,
-        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{args.workload}: {args.steps} single MLEM iterations (of K={cfg.K}), 1 frame"},
+        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": cores, "kind": "oracle", "cpu": cpu_model(),
+                         "sample": f"{args.workload}: {args.steps} single MLEM iterations (of K={cfg.K}), 1 frame, "
+                                   f"{cores} OpenMP threads"},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: start N ranks with torch.distributed.run on
+    127.0.0.1 so that the line reports what N GPUs did (never a silent single-GPU run)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -170,6 +230,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+        return 2
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -180,7 +243,7 @@ def main():
     geom = cfg.geom
     K = cfg.K if args.iters is None else args.iters
     taps = syn.paper_taps(cfg)
-    mode = args.mode if world > 1 else "frames"
+    mode = args.mode
     if args.frames is not None:
         frames = args.frames
     elif cfg.frames > 1:
@@ -217,14 +280,16 @@ def main():
     ws = plan.workspace(frames)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)     # > 126 MB L2
     stream = torch.cuda.current_stream()
-    ghat = torch.empty(geom.n, dtype=torch.float32, device=dev)
 
-    def allreduce(t):
-        dist.all_reduce(t)
+    comm = ws_sh = None
+    if mode == "bands":
+        comm = dmod.make_comm(local)                      # NCCL communicator owned by libctis
+        ws_sh = plan.band_sharded_workspace(comm)
 
     def one_step(fb):
         if mode == "bands":
-            dmod.mlem_band_sharded(plan, g, fb, K, allreduce, ghat=ghat, ws=ws)
+            # partial forward -> reduce-scatter -> slice ratio -> all-gather -> back update, K times, one graph
+            dmod.mlem_band_sharded_nccl(plan, comm, g, fb, K, ws=ws_sh)
         else:
             plan.mlem(g, fb, K, ws=ws)
 
@@ -232,7 +297,7 @@ def main():
         flush.zero_()
         fbufs[i].fill_(1.0)
         one_step(fbufs[i])
-    launches_per_step = plan.last_launch_count() * (K if mode == "bands" else 1)
+    launches_per_step = plan.last_launch_count()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -367,13 +432,8 @@ def main():
 
     # ---- CPU oracle beside it (rank 0, N = 1 only, bounded sample)
     if line is not None and world == 1 and not args.no_cpu_baseline:
-        import oracle
-        iters_cpu = 2 if geom.m * int(taps.ptr[1]) > 1e8 else max(1, min(K, int(2e8 // (geom.m * int(taps.ptr[1]) + 1))))
         gnp = (g if frames == 1 else g[0]).double().cpu().numpy()
-        t_cpu = cpu_oracle_iterations(cfg, taps, gnp, iters_cpu)
-        line["cpu_baseline"] = {"value": iters_cpu / t_cpu, "unit": "iterations/s", "cores": 1, "kind": "oracle",
-                                "sample": f"{args.workload}: {iters_cpu} MLEM iterations (of K={K}), 1 frame, "
-                                          f"{t_cpu:.1f} s single-threaded"}
+        line["cpu_baseline"] = cpu_baseline(cfg, taps, gnp, K, args.workload)
     if line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

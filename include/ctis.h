@@ -200,6 +200,46 @@ CTIS_API ctis_status ctis_smart(ctis_plan plan, const float* g, float* f, int64_
 CTIS_API ctis_status ctis_mlem_monitored(ctis_plan plan, const float* g, float* f, int max_iters, double rel_tol,
                                          void* ws, double* ll, int* iters_done, ctis_stream stream);
 
+/* ---- Latency mode over NCCL ---------------------------------------------
+ * H = (H_1 ... H_w) is a row of per-band block columns (Eq. 3), so with the bands
+ * split over P ranks g_hat = H f = sum over ranks of H_shard f_shard.  One iteration of
+ * ctis_mlem_band_sharded on every rank (Alg. 1):
+ *   X <- 0 on the exchange range; X += H_shard f_shard (partial forward, lines 6-7);
+ *   reduce-scatter(X) (NCCL, sum): rank k holds g_hat on its slice k of the exchange range;
+ *   X_k <- g_k (/) X_k on that slice (line 8; 0 where g_hat <= 0, reading R4);
+ *   all-gather(X): every rank holds r = g (/) g_hat on the whole range;
+ *   f_shard <- f_shard (.) (H_shard^T r) (/) h (lines 9-12).
+ * The exchange range is the contiguous FPA index range [lo, hi] that any tap of ANY band can reach
+ * (min_t o_t .. max_t o_t + E(l-1); the whole [0, n) if a tap wraps), split into P equal 16-byte
+ * aligned slices: pixels outside it are zero in every partial and never read.  All `iters`
+ * iterations are enqueued as ONE CUDA graph (kernels and NCCL calls), replayed without host
+ * synchronisation.  NCCL is loaded at run time (libnccl.so.2); without it these calls return
+ * CTIS_ERR_UNSUPPORTED. */
+typedef struct ctis_comm_s* ctis_comm;
+
+/* 128-byte NCCL unique id, created on one rank and broadcast to all (the caller's side channel). */
+CTIS_API ctis_status ctis_comm_unique_id(uint8_t id[128]);
+
+/* Collective: every rank of the group calls it with the same id and nranks, its own rank and the
+ * device its shard plans use.  *out is owned by the caller (ctis_comm_destroy). */
+CTIS_API ctis_status ctis_comm_create(int nranks, int rank, const uint8_t id[128], int device, ctis_comm* out);
+CTIS_API void ctis_comm_destroy(ctis_comm comm);
+
+/* Device workspace bytes for ctis_mlem_band_sharded on this shard plan and communicator (the
+ * exchange buffer X, >= n floats, 16-byte aligned). */
+CTIS_API size_t ctis_band_sharded_workspace_bytes(ctis_plan shard, ctis_comm comm);
+
+/* `iters` band-sharded MLEM iterations (above).  Collective over `comm`: every rank calls it with
+ * its own shard plan (band ranges partitioning [0, w), all created from the same full tap CSR).
+ * g: DEVICE, n floats, the full measurement (replicated on every rank; read only).
+ * f_local: DEVICE, m_local floats of this rank's bands, updated in place (f^(1) in, f^(iters+1) out).
+ * ws: DEVICE, ctis_band_sharded_workspace_bytes bytes.  Stream-ordered on `stream`.
+ * Errors: CTIS_ERR_INVALID_ARGUMENT (NULL / misaligned pointers, iters < 0, a plan of another
+ * device), CTIS_ERR_UNSUPPORTED (no NCCL), CTIS_ERR_CUDA (CUDA or NCCL failure, text in
+ * ctis_last_error).  iters = 0 leaves f_local unchanged. */
+CTIS_API ctis_status ctis_mlem_band_sharded(ctis_plan shard, ctis_comm comm, const float* g, float* f_local,
+                                            int iters, void* ws, ctis_stream stream);
+
 /* End-to-end convenience on HOST buffers: copies g_host[frames][n] and
  * f_host[frames][m] (f0) to plan-owned device buffers, runs ctis_mlem_batched,
  * copies f back into f_host and synchronises `stream` before returning.

@@ -49,6 +49,11 @@ _SIGS = {
     "ctis_forward_ratio": ([_P, _P, _P, _P, _P], _int),
     "ctis_back_update": ([_P, _P, _P, _P], _int),
     "ctis_mlem_host": ([_P, _P, _P, _i64, _int, _P], _int),
+    "ctis_comm_unique_id": ([_P], _int),
+    "ctis_comm_create": ([_int, _int, _P, _int, _P], _int),
+    "ctis_comm_destroy": ([_P], None),
+    "ctis_band_sharded_workspace_bytes": ([_P, _P], ctypes.c_size_t),
+    "ctis_mlem_band_sharded": ([_P, _P, _P, _P, _int, _P, _P], _int),
     "ctis_last_launch_count": ([_P], _i64),
     "ctis_last_error": ([], ctypes.c_char_p),
     "ctis_version": ([], ctypes.c_char_p),
@@ -64,6 +69,37 @@ EXPORTED = tuple(_SIGS)
 OK, ERR_INVALID_ARGUMENT, ERR_DIMENSION, ERR_TAP, ERR_ZERO_SENSITIVITY, ERR_DATA, ERR_CUDA, \
     ERR_OUT_OF_MEMORY, ERR_UNSUPPORTED = range(9)
 OPT_VALIDATE_DATA, OPT_USE_GRAPH, OPT_PROJECTOR = 1, 2, 3
+
+
+def comm_unique_id() -> bytes:
+    """128-byte NCCL unique id (ctis_comm_unique_id) for Comm(); create on one rank, broadcast to all."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(_lib.ctis_comm_unique_id(buf), "ctis_comm_unique_id")
+    return bytes(buf)
+
+
+class Comm:
+    """NCCL communicator owned by libctis (ctis_comm_create): the latency mode's exchange."""
+
+    def __init__(self, nranks: int, rank: int, uid: bytes, device: int = 0):
+        if len(uid) != 128:
+            raise ValueError("uid must be 128 bytes")
+        self._h = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        _check(_lib.ctis_comm_create(int(nranks), int(rank), buf, int(device), ctypes.byref(self._h)),
+               "ctis_comm_create")
+        self.nranks, self.rank, self.device = int(nranks), int(rank), int(device)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            _lib.ctis_comm_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class CtisError(RuntimeError):
@@ -258,6 +294,21 @@ class Plan:
         _check(_lib.ctis_back_update(self._h, _dev_ptr(r, self.n, "r"), _dev_ptr(f, self.m, "f"),
                                      _stream_handle(stream)), "ctis_back_update")
         return f
+
+    def band_sharded_workspace(self, comm: "Comm"):
+        import torch
+        nbytes = int(_lib.ctis_band_sharded_workspace_bytes(self._h, comm._h))
+        return torch.empty(nbytes // 4, dtype=torch.float32, device=f"cuda:{self.device}")
+
+    def mlem_band_sharded(self, comm: "Comm", g, f_local, iters: int, ws=None, stream=None):
+        """Latency mode (ctis_mlem_band_sharded): `iters` iterations of partial forward -> NCCL
+        reduce-scatter -> ratio on this rank's slice -> all-gather -> back update, as one CUDA graph.
+        Collective over `comm`; g: full n floats; f_local: this shard's m floats, in place."""
+        ws = self.band_sharded_workspace(comm) if ws is None else ws
+        _check(_lib.ctis_mlem_band_sharded(self._h, comm._h, _dev_ptr(g, self.n, "g"), _dev_ptr(f_local, self.m, "f"),
+                                           int(iters), ctypes.c_void_p(ws.data_ptr()), _stream_handle(stream)),
+               "ctis_mlem_band_sharded")
+        return f_local
 
     def back_update_from_ghat(self, g, g_hat, f, ws=None, stream=None):
         """Latency mode: r = g/g_hat (all-reduced), f_shard <- f_shard (.) H_shard^T r (/) h."""

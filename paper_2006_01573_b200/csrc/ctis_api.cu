@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/ctis.h"
+#include "ctis_comm.h"
 #include "ctis_internal.h"
 #include "ctis_fft.h"
 #include "ctis_kernels.h"
@@ -105,6 +106,7 @@ struct ctis_plan_s {
   int device = 0;
   int a = 0, alpha = 0, w = 0, gamma = 0, xi = 0, n = 0, ell = 0, m = 0;
   int64_t band_begin = 0, band_end = 0, total_taps = 0;
+  int64_t ex_lo = 0, ex_hi = 0;  // FPA index range any tap of any band reaches (latency-mode exchange)
   bool shard = false, validate = true, use_graph = true;
   bool tma_f = false, tma_b = false;
   int back_nb = kBackBandsMax;
@@ -125,6 +127,7 @@ struct ctis_plan_s {
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<MonKey, cudaGraphExec_t> mon_graphs;
+  std::map<GraphKey, cudaGraphExec_t> shard_graphs;  // band-sharded iterations (key.frames = comm id)
   int projector = 0;                 // CTIS_OPT_PROJECTOR: 0 taps (default), 1 the paper's FFT route
   ctis::FftState* fft = nullptr;     // created when the FFT projector is selected
   std::vector<std::vector<std::pair<int64_t, float>>> band_taps;  // (offset, weight) per local band
@@ -136,6 +139,7 @@ struct ctis_plan_s {
     DeviceGuard dg(device);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : mon_graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : shard_graphs) cudaGraphExecDestroy(kv.second);
     ctis::fft_destroy(fft);
     if (side) cudaStreamDestroy(side);
     if (ev_in) cudaEventDestroy(ev_in);
@@ -146,6 +150,12 @@ struct ctis_plan_s {
     for (void* p : {(void*)d_hband, (void*)d_flag, (void*)d_g, (void*)d_f, d_ws})
       if (p) cudaFree(p);
   }
+};
+
+struct ctis_comm_s {
+  void* nccl = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+  ~ctis_comm_s() { ctis::nccl_comm_destroy(nccl); }
 };
 
 namespace {
@@ -752,6 +762,19 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
     if (!((float)hs > 0.f) || !std::isfinite((float)hs)) return fail(CTIS_ERR_ZERO_SENSITIVITY, "h_lambda not > 0");
     hband.push_back((float)hs);
   }
+  // exchange range of the latency mode: every pixel a tap of any band can reach, E(j) <= E(l-1)
+  int64_t ex_lo = n, ex_hi = -1;
+  {
+    const int64_t emax = (a - 1) + gamma * (alpha - 1);
+    for (int64_t t = 0; t < tap_ptr[w]; ++t) {
+      ex_lo = std::min(ex_lo, tap_offset[t]);
+      ex_hi = std::max(ex_hi, tap_offset[t] + emax);
+    }
+    if (ex_hi >= n) {  // some tap wraps past n (Eq. 7): the whole FPA
+      ex_lo = 0;
+      ex_hi = n - 1;
+    }
+  }
   int ndev = 0;
   CTIS_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
   if (device < 0 || device >= ndev) return fail(CTIS_ERR_INVALID_ARGUMENT, "device ordinal out of range");
@@ -766,6 +789,8 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
   p->shard = shard;
   p->band_begin = b0;
   p->band_end = b1;
+  p->ex_lo = ex_lo;
+  p->ex_hi = ex_hi;
   p->a = (int)a;
   p->alpha = (int)alpha;
   p->w = (int)(b1 - b0);
@@ -1166,9 +1191,136 @@ ctis_status run_mlem_monitored(ctis_plan_s& P, const float* g, float* f, int max
   return CTIS_OK;
 }
 
+// Latency-mode exchange layout (include/ctis.h): base B (16-byte aligned) and per-rank slice S (floats,
+// multiple of 4) covering the plan's exchange range [ex_lo, ex_hi]; X holds >= max(n, B + P*S) floats.
+struct Exchange {
+  int64_t base, slice, floats;
+};
+Exchange exchange_layout(const ctis_plan_s& P, const ctis_comm_s& C) {
+  Exchange e;
+  e.base = P.ex_lo & ~int64_t(3);
+  const int64_t len = P.ex_hi + 1 - e.base;
+  e.slice = ((len + C.nranks - 1) / C.nranks + 3) & ~int64_t(3);
+  e.floats = (std::max<int64_t>(P.n, e.base + e.slice * C.nranks) + 3) & ~int64_t(3);
+  return e;
+}
+
+// One band-sharded MLEM reconstruction on stream s (kernels + NCCL calls; capturable).
+ctis_status enqueue_band_sharded(ctis_plan_s& P, ctis_comm_s& C, const float* g, float* f, float* X, int iters,
+                                 cudaStream_t s, int64_t* cnt) {
+  const Exchange ex = exchange_layout(P, C);
+  float* slice = X + ex.base + (int64_t)C.rank * ex.slice;
+  const int64_t s0 = ex.base + (int64_t)C.rank * ex.slice;
+  const int64_t ratio_count = s0 >= P.n ? 0 : std::min<int64_t>(ex.slice, P.n - s0);
+  std::string err;
+  CTIS_CUDA(cudaMemsetAsync(X, 0, sizeof(float) * (size_t)ex.floats, s), "exchange buffer memset");
+  for (int k = 0; k < iters; ++k) {
+    if (k > 0) CTIS_CUDA(cudaMemsetAsync(X + ex.base, 0, sizeof(float) * (size_t)(ex.slice * C.nranks), s), "memset");
+    CTIS_CUDA(enqueue_forward(P, f, X, 1, s, cnt), "partial forward");
+    if (!nccl_reduce_scatter_f32(X + ex.base, slice, (size_t)ex.slice, C.nccl, s, &err)) return fail(CTIS_ERR_CUDA, err);
+    if (ratio_count > 0) {
+      CTIS_CUDA(launch_ratio(g + s0, slice, slice, ratio_count, false, s), "slice ratio");
+      ++*cnt;
+    }
+    if (!nccl_all_gather_f32(slice, X + ex.base, (size_t)ex.slice, C.nccl, s, &err)) return fail(CTIS_ERR_CUDA, err);
+    CTIS_CUDA(enqueue_back(P, X, f, 1, 1, s, cnt), "back update");
+  }
+  return CTIS_OK;
+}
+
+ctis_status run_band_sharded(ctis_plan_s& P, ctis_comm_s& C, const float* g, float* f, int iters, void* ws,
+                             cudaStream_t s) {
+  if (iters < 0) return fail(CTIS_ERR_INVALID_ARGUMENT, "iters < 0");
+  if (C.device != P.device) return fail(CTIS_ERR_INVALID_ARGUMENT, "communicator and plan are on different devices");
+  ctis_status st = check_ptrs({g, f, ws});
+  if (st) return st;
+  DeviceGuard dg(P.device);
+  P.last_launches = 0;
+  if (iters == 0) return CTIS_OK;
+  float* X = static_cast<float*>(ws);
+  int64_t cnt = 0;
+  if (!P.use_graph) return enqueue_band_sharded(P, C, g, f, X, iters, s, &P.last_launches);
+  GraphKey key{g, f, ws, (int64_t)reinterpret_cast<intptr_t>(&C), iters, 2};
+  auto it = P.shard_graphs.find(key);
+  if (it == P.shard_graphs.end()) {
+    if (P.shard_graphs.size() >= 8) {
+      for (auto& kv : P.shard_graphs) cudaGraphExecDestroy(kv.second);
+      P.shard_graphs.clear();
+    }
+    cudaGraph_t graph = nullptr;
+    CTIS_CUDA(cudaStreamBeginCapture(P.side, cudaStreamCaptureModeThreadLocal), "begin capture");
+    ctis_status est = enqueue_band_sharded(P, C, g, f, X, iters, P.side, &cnt);
+    cudaError_t e2 = cudaStreamEndCapture(P.side, &graph);
+    if (est) {
+      if (graph) cudaGraphDestroy(graph);
+      return est;
+    }
+    if (e2 != cudaSuccess) return cuda_fail(e2, "end capture (band-sharded)");
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e, "graph instantiate (band-sharded)");
+    it = P.shard_graphs.emplace(key, exec).first;
+  } else {
+    cnt = (int64_t)iters * ((int64_t)P.fwd.size() + (int64_t)P.back.size() + 1);
+  }
+  CTIS_CUDA(cudaEventRecord(P.ev_in, s), "event record");
+  CTIS_CUDA(cudaStreamWaitEvent(P.side, P.ev_in, 0), "stream wait");
+  CTIS_CUDA(cudaGraphLaunch(it->second, P.side), "graph launch");
+  CTIS_CUDA(cudaEventRecord(P.ev_out, P.side), "event record");
+  CTIS_CUDA(cudaStreamWaitEvent(s, P.ev_out, 0), "stream wait");
+  P.last_launches = cnt;
+  return CTIS_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+ctis_status ctis_comm_unique_id(uint8_t id[128]) {
+  if (!id) return fail(CTIS_ERR_INVALID_ARGUMENT, "id is NULL");
+  std::string err;
+  if (!nccl_available(&err)) return fail(CTIS_ERR_UNSUPPORTED, err);
+  if (!nccl_unique_id(id, &err)) return fail(CTIS_ERR_CUDA, err);
+  return CTIS_OK;
+}
+
+ctis_status ctis_comm_create(int nranks, int rank, const uint8_t id[128], int device, ctis_comm* out) {
+  if (!out || !id) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(CTIS_ERR_INVALID_ARGUMENT, "rank / nranks out of range");
+  std::string err;
+  if (!nccl_available(&err)) return fail(CTIS_ERR_UNSUPPORTED, err);
+  int ndev = 0;
+  CTIS_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) return fail(CTIS_ERR_INVALID_ARGUMENT, "device ordinal out of range");
+  DeviceGuard dg(device);
+  CTIS_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  auto* c = new ctis_comm_s();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  if (!nccl_comm_init(&c->nccl, nranks, rank, id, &err)) {
+    delete c;
+    return fail(CTIS_ERR_CUDA, err);
+  }
+  *out = c;
+  return CTIS_OK;
+}
+
+void ctis_comm_destroy(ctis_comm comm) { delete comm; }
+
+size_t ctis_band_sharded_workspace_bytes(ctis_plan p, ctis_comm c) {
+  if (!p || !c) return 0;
+  return sizeof(float) * (size_t)exchange_layout(*p, *c).floats;
+}
+
+ctis_status ctis_mlem_band_sharded(ctis_plan p, ctis_comm c, const float* g, float* f_local, int iters, void* ws,
+                                   ctis_stream stream) {
+  if (!p || !c) return fail(CTIS_ERR_INVALID_ARGUMENT, "NULL plan or communicator");
+  std::lock_guard<std::mutex> lk(p->mu);
+  return run_band_sharded(*p, *c, g, f_local, iters, ws, (cudaStream_t)stream);
+}
 
 ctis_status ctis_plan_create(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi, const int64_t* tap_ptr,
                              const int64_t* tap_offset, const float* tap_weight, int device, ctis_plan* out) {

@@ -72,6 +72,62 @@ def mlem_band_sharded(plan, g, f_local, iters: int, all_reduce: Callable, ghat=N
     return f_local
 
 
+def make_comm(device: int, group=None):
+    """A libctis NCCL communicator over the torch.distributed group: rank 0 creates the unique id,
+    the group broadcasts it (the side channel NCCL needs), every rank calls ctis_comm_create."""
+    import torch.distributed as dist
+
+    import paper_2006_01573_b200 as ctis
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [ctis.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return ctis.Comm(world, rank, obj[0], device)
+
+
+def mlem_band_sharded_nccl(plan, comm, g, f_local, iters: int, ws=None, stream=None):
+    """Latency mode with the exchange inside libctis (ctis_mlem_band_sharded): per iteration partial
+    forward -> reduce-scatter of g_hat -> ratio on this rank's slice -> all-gather of r -> back update,
+    all `iters` iterations replayed as one CUDA graph (NCCL calls captured with the kernels)."""
+    return plan.mlem_band_sharded(comm, g, f_local, iters, ws=ws, stream=stream)
+
+
+def exchange_slices(lo: int, hi: int, n: int, parts: int) -> Tuple[int, int, int]:
+    """The exchange layout of ctis_mlem_band_sharded (include/ctis.h): base (16-byte aligned), per-rank
+    slice (floats, multiple of 4) covering [lo, hi], and the exchange buffer length in floats."""
+    base = lo & ~3
+    length = hi + 1 - base
+    slice_ = ((length + parts - 1) // parts + 3) & ~3
+    floats = (max(n, base + slice_ * parts) + 3) & ~3
+    return base, slice_, floats
+
+
+def mlem_band_sharded_exchange(forward_partial: Callable, ratio_slice: Callable, back_update: Callable, g, f_local,
+                               iters: int, lo: int, hi: int, rank: int, parts: int,
+                               reduce_scatter: Callable, all_gather: Callable, X):
+    """The exchange schedule of ctis_mlem_band_sharded written with pluggable steps and collectives —
+    the host-level specification the C implementation follows, exercised on CPU with gloo
+    (tests/test_distributed_gloo.py).  X: exchange buffer of exchange_slices(...)[2] elements.
+
+    per iteration: X[base:base+P*S] = 0; X += partial forward; reduce-scatter -> own slice;
+    slice <- g_slice (/) slice; all-gather -> r on the whole range; f_local <- back_update(r)."""
+    n = g.shape[0]
+    base, S, floats = exchange_slices(lo, hi, n, parts)
+    assert X.shape[0] >= floats
+    s0 = base + rank * S
+    cnt = 0 if s0 >= n else min(S, n - s0)
+    X.zero_()
+    for _ in range(int(iters)):
+        X[base:base + S * parts].zero_()
+        forward_partial(f_local, X)
+        mine = X[s0:s0 + S]
+        reduce_scatter(mine, X[base:base + S * parts])
+        if cnt:
+            ratio_slice(g[s0:s0 + cnt], mine[:cnt])
+        all_gather(X[base:base + S * parts], mine)
+        back_update(X[:n], f_local)
+    return f_local
+
+
 def mlem_band_sharded_local(plans: Sequence, g, f_locals: Sequence, iters: int):
     """All shards of a latency-mode run on ONE device: the all-reduce is a plain on-device sum.
 

@@ -88,6 +88,70 @@ def test_band_sharded_mlem_gloo_world2_matches_single_process(oracle_lib):
     np.testing.assert_allclose(f_sharded, want, rtol=1e-12, atol=1e-14)
 
 
+def _exchange_worker(rank, world, port, region, results):
+    """The reduce-scatter / slice-ratio / all-gather schedule of ctis_mlem_band_sharded with real gloo
+    collectives and the oracle as the shard projector."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_2006_01573_b200 import distributed as dm
+    geom = syn.Geometry(9, 7, 5, 40, 30)
+    taps = (syn.paper_taps(geom, R=1, seed=2) if region == "paper"
+            else syn.random_taps(geom, (2, 6), seed=8, region=region))
+    g = torch.from_numpy(oracle.forward(geom, taps, syn.scene_blobs(geom)))
+    emax = (geom.a - 1) + geom.gamma * (geom.alpha - 1)
+    lo, hi = int(taps.offset.min()), int(taps.offset.max()) + emax
+    if hi >= geom.n:
+        lo, hi = 0, geom.n - 1
+    b0, b1 = dm.band_partition(geom.w, world)[rank]
+    shard = OracleShard(geom, taps, b0, b1)
+    X = torch.empty(dm.exchange_slices(lo, hi, geom.n, world)[2], dtype=torch.float64)
+
+    def forward_partial(f, X):
+        X[:geom.n] += torch.from_numpy(oracle.forward(shard.geom, shard.taps, f.numpy()))
+
+    def ratio_slice(gs, xs):
+        gh = xs.numpy().copy()
+        xs.copy_(torch.from_numpy(np.where(gh > 0, gs.numpy() / np.where(gh > 0, gh, 1.0), 0.0)))
+
+    def back_update(r, f):
+        z = oracle.backproject(shard.geom, shard.taps, r.numpy())
+        f.copy_(torch.from_numpy(f.numpy() * z / shard.h))
+
+    f = torch.ones(shard.m, dtype=torch.float64)
+    dm.mlem_band_sharded_exchange(forward_partial, ratio_slice, back_update, g, f, 12, lo, hi, rank, world,
+                                  reduce_scatter=lambda out, inp: dist.reduce_scatter_tensor(out, inp),
+                                  all_gather=lambda out, inp: dist.all_gather_into_tensor(out, inp), X=X)
+    parts = [None] * world
+    dist.all_gather_object(parts, f.numpy())
+    if rank == 0:
+        results.put(np.concatenate(parts))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,region", [(2, "paper"), (3, "any"), (2, "nowrap")])
+def test_reduce_scatter_exchange_gloo_matches_single_process(oracle_lib, world, region):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    mp.start_processes(_exchange_worker, args=(world, _free_port(), region, q), nprocs=world, start_method="spawn",
+                       join=True)
+    f_sharded = q.get()
+    geom = syn.Geometry(9, 7, 5, 40, 30)
+    taps = (syn.paper_taps(geom, R=1, seed=2) if region == "paper"
+            else syn.random_taps(geom, (2, 6), seed=8, region=region))
+    g = oracle_lib.forward(geom, taps, syn.scene_blobs(geom))
+    want = oracle_lib.mlem(geom, taps, g, np.ones(geom.m), 12)
+    np.testing.assert_allclose(f_sharded, want, rtol=1e-12, atol=1e-14)
+
+
+def test_exchange_layout():
+    from paper_2006_01573_b200 import distributed as dm
+    base, S, floats = dm.exchange_slices(5, 4_194_303, 4_194_304, 8)
+    assert base == 4 and S % 4 == 0 and base + 8 * S >= 4_194_304 and floats >= 4_194_304 and floats % 4 == 0
+    base, S, floats = dm.exchange_slices(0, 99, 100, 3)
+    assert (base, S, floats) == (0, 36, 108)
+
+
 def test_partitions():
     from paper_2006_01573_b200 import distributed as dm
     assert dm.band_partition(100, 8) == [(0, 13), (13, 26), (26, 39), (39, 52), (52, 64), (64, 76), (76, 88), (88, 100)]

@@ -292,6 +292,81 @@ def test_band_shards_wrapping_taps_vs_oracle(ctis, oracle_lib, dev, nshards):
     check(torch.cat(out).cpu().numpy(), want, MLEM_TOL, f"wrapping band-sharded MLEM ({nshards} shards)")
 
 
+# ------------------------------------------------------------------ latency mode through libctis + NCCL
+@pytest.mark.parametrize("case", ["C2", "C3", "wrap"])
+def test_band_sharded_nccl_single_rank_vs_oracle(ctis, oracle_lib, dev, case):
+    """ctis_mlem_band_sharded on a one-rank NCCL communicator (this box has one GPU): the whole
+    schedule — exchange-range slicing, reduce-scatter, slice ratio, all-gather, back update, captured
+    with the NCCL calls in one CUDA graph — against the oracle."""
+    if case == "wrap":
+        geom = syn.Geometry(33, 17, 6, 70, 45)
+        taps = syn.random_taps(geom, (2, 9), seed=77, region="any")
+        K, ftrue = 25, syn.scene_random(geom, seed=3, lo=0.1)
+    else:
+        cfg = syn.config(case)
+        geom, taps, K, ftrue = cfg.geom, syn.paper_taps(cfg), cfg.K, syn.scene_blobs(cfg.geom)
+    g_np = oracle_lib.forward(geom, taps, ftrue).astype(np.float32)
+    try:
+        comm = ctis.Comm(1, 0, ctis.comm_unique_id(), 0)
+    except ctis.CtisError as e:
+        pytest.skip(f"NCCL unavailable: {e}")
+    shard = ctis.Plan.from_geometry(geom, taps, band_range=(0, geom.w))
+    f = torch.ones(geom.m, device=dev)
+    shard.mlem_band_sharded(comm, cuda(g_np, dev), f, K)
+    launches = shard.last_launch_count()
+    want = oracle_lib.mlem(geom, taps, g_np, np.ones(geom.m), K)
+    check(f.cpu().numpy(), want, MLEM_TOL, f"{case} band-sharded NCCL (1 rank) K={K}")
+    assert launches >= 3 * K
+    f2 = torch.ones(geom.m, device=dev)          # replay of the cached graph
+    shard.mlem_band_sharded(comm, cuda(g_np, dev), f2, K)
+    assert rel(f2.cpu().numpy(), f.cpu().numpy()) <= 1e-6
+    f3 = torch.ones(geom.m, device=dev)
+    shard.mlem_band_sharded(comm, cuda(g_np, dev), f3, 0)
+    assert bool((f3 == 1).all())
+    comm.close()
+
+
+def _nccl_worker(rank, world, port, q):
+    import os as _os
+    import torch.distributed as tdist
+    _os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    tdist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device(f"cuda:{rank}"))
+    import paper_2006_01573_b200 as m
+    from paper_2006_01573_b200 import distributed as dm
+    import oracle
+    cfg = syn.config("C2")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    g_np = oracle.forward(geom, taps, syn.scene_blobs(geom)).astype(np.float32)
+    b0, b1 = dm.band_partition(geom.w, world)[rank]
+    shard = m.Plan.from_geometry(geom, taps, device=rank, band_range=(b0, b1))
+    comm = dm.make_comm(rank)
+    f = torch.ones(shard.m, device=f"cuda:{rank}")
+    shard.mlem_band_sharded(comm, torch.from_numpy(g_np).cuda(rank), f, cfg.K)
+    parts = [None] * world
+    tdist.all_gather_object(parts, f.cpu().numpy())
+    if rank == 0:
+        q.put(np.concatenate(parts))
+    tdist.destroy_process_group()
+
+
+def test_band_sharded_nccl_multi_gpu_vs_oracle(ctis, oracle_lib):
+    """Two ranks on two GPUs (runs only where >= 2 GPUs are visible)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (this gpurun box exposes one)")
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    q = mp.get_context("spawn").SimpleQueue()
+    mp.start_processes(_nccl_worker, args=(2, port, q), nprocs=2, start_method="spawn", join=True)
+    cfg = syn.config("C2")
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    g_np = oracle_lib.forward(geom, taps, syn.scene_blobs(geom)).astype(np.float32)
+    check(q.get(), oracle_lib.mlem(geom, taps, g_np, np.ones(geom.m), cfg.K), MLEM_TOL, "C2 band-sharded NCCL 2 GPUs")
+
+
 # ------------------------------------------------------------------ end-to-end host path
 def test_mlem_host_path_matches_device_path(ctis, dev):
     cfg = syn.config("C2")
