@@ -78,12 +78,19 @@ typedef enum {
                                    0: skip (the call is then fully asynchronous). */
   CTIS_OPT_USE_GRAPH = 2,       /* 1 (default): ctis_mlem* replay a captured CUDA graph of the
                                    iterations; 0: launch kernels directly on `stream`. */
-  CTIS_OPT_PROJECTOR = 3        /* 0 (default): the tap projector.  1: the paper's own Fourier route
+  CTIS_OPT_PROJECTOR = 3,       /* 0 (default): the tap projector.  1: the paper's own Fourier route
                                    (Eqs. 13 and 17 with cuFFT, d_i = F c_i precomputed; Alg. 1
                                    lines 6-11) for every ctis_forward / _backproject / _mlem* call on the
                                    plan — a comparator arm.  Allocates O(w n) complex
                                    scratch owned by the plan (CTIS_ERR_OUT_OF_MEMORY if it does not fit):
                                    calls on one plan must then not run concurrently on different streams. */
+  CTIS_OPT_FUSED_RATIO = 4      /* 1: ctis_mlem / ctis_mlem_batched / ctis_smart on plans with
+                                   persistent (TMA) forward kernels run two kernels per iteration: the
+                                   forward's last launch is cooperative and, after a grid-wide barrier,
+                                   turns g_hat into r = g (/) g_hat in place (Alg. 1 line 8); the back
+                                   kernel zeroes the other workspace half for the next forward.
+                                   0 (default): three kernels per iteration (separate ratio pass),
+                                   measured faster on B200 (C4 149.5 vs 150.8 us per iteration). */
 } ctis_option;
 
 /* Create a plan for the full operator H (all w bands).

@@ -19,7 +19,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libctis.so")
+LIB_PATH = os.environ.get("CTIS_LIB_PATH") or os.path.join(_HERE, "libctis.so")  # override: experiment builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libctis.so not built at {LIB_PATH}: run `make` (or __graft_entry__.build()). "
@@ -68,7 +68,7 @@ EXPORTED = tuple(_SIGS)
 # status codes (include/ctis.h)
 OK, ERR_INVALID_ARGUMENT, ERR_DIMENSION, ERR_TAP, ERR_ZERO_SENSITIVITY, ERR_DATA, ERR_CUDA, \
     ERR_OUT_OF_MEMORY, ERR_UNSUPPORTED = range(9)
-OPT_VALIDATE_DATA, OPT_USE_GRAPH, OPT_PROJECTOR = 1, 2, 3
+OPT_VALIDATE_DATA, OPT_USE_GRAPH, OPT_PROJECTOR, OPT_FUSED_RATIO = 1, 2, 3, 4
 
 
 def comm_unique_id() -> bytes:

@@ -126,6 +126,7 @@ struct ctis_plan_s {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<GraphKey, int64_t> graph_launches;  // kernels inside each cached graph
   std::map<MonKey, cudaGraphExec_t> mon_graphs;
   std::map<GraphKey, cudaGraphExec_t> shard_graphs;  // band-sharded iterations (key.frames = comm id)
   int projector = 0;                 // CTIS_OPT_PROJECTOR: 0 taps (default), 1 the paper's FFT route
@@ -133,6 +134,8 @@ struct ctis_plan_s {
   std::vector<std::vector<std::pair<int64_t, float>>> band_taps;  // (offset, weight) per local band
   std::vector<float> inv_h;          // 1 / h_lambda per local band
   int64_t last_launches = 0;
+  bool fused_ratio = false;    // CTIS_OPT_FUSED_RATIO (measured slower: DESIGN.md)
+  unsigned* d_gbar = nullptr;  // grid barrier word of the cooperative forward launches
   std::mutex mu;
 
   ~ctis_plan_s() {
@@ -147,7 +150,7 @@ struct ctis_plan_s {
     for (auto* pages : {&fwd, &back})
       for (Page& p : *pages)
         if (p.lib) cudaLibraryUnload(p.lib);
-    for (void* p : {(void*)d_hband, (void*)d_flag, (void*)d_g, (void*)d_f, d_ws})
+    for (void* p : {(void*)d_hband, (void*)d_flag, (void*)d_g, (void*)d_f, d_ws, (void*)d_gbar})
       if (p) cudaFree(p);
   }
 };
@@ -823,6 +826,8 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
     e = cudaMalloc(&p->d_hband, sizeof(float) * p->w);
     if (e == cudaSuccess) e = cudaMemcpy(p->d_hband, hloc.data(), sizeof(float) * p->w, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_flag, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_gbar, 64);
+    if (e == cudaSuccess) e = cudaMemset(p->d_gbar, 0, 64);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming);
@@ -916,19 +921,36 @@ cudaError_t make_tensor_map(CUtensorMap* tm, bool forward, const ctis_plan_s& P,
 
 // Launch with programmatic stream serialization (PDL): the kernel may start while its predecessor
 // drains; it waits for the predecessor's results with griddepcontrol.wait (ctis_tables.cu pdl_enter).
-cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s) {
+cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s,
+                       bool cooperative = false) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() && !cooperative ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeCooperative;  // every CTA resident: the grid barrier cannot deadlock
+#ifdef CTIS_NO_COOP
+  attr[1].val.cooperative = 0;  // measurement only: the grid barrier relies on co-residency
+#else
+  attr[1].val.cooperative = cooperative ? 1 : 0;
+#endif
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
+
+// Fused extras of a projection launch: forward — ratio in place after a grid barrier (last page);
+// back — zero the next iteration's accumulator (first page).
+struct Fuse {
+  int ratio_mode = 0;
+  const float* meas = nullptr;
+  long long ratio_count = 0;
+  float* zero_buf = nullptr;
+  long long zero_count = 0;
+};
 
 int debug_flags() {
   static int v = [] {
@@ -940,7 +962,7 @@ int debug_flags() {
 
 cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const float* src, float* dst,
                          long long src_frame, long long dst_frame, int frames, int mode, cudaStream_t s,
-                         int64_t* count) {
+                         int64_t* count, const Fuse* fuse = nullptr) {
   if (pages.empty()) return cudaSuccess;
   const bool fwd = pages[0].forward;
   const bool tma = fwd ? P.tma_f : P.tma_b;
@@ -954,7 +976,8 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
   const int cap = fwd ? kFwdWinFloats : kBackWinFloats;
   int slot = tma ? (box_r * box_c + 31) / 32 * 32 : cap;
   TabArgs A{src, dst, src_frame, dst_frame, P.a, P.alpha, P.gamma, P.xi, P.n, P.ell, mode, bias, nsub,
-            slot, box_r, box_c, (unsigned)(4 * box_r * box_c), debug_flags(), frames, P.nowrap ? 1 : 0};
+            slot, box_r, box_c, (unsigned)(4 * box_r * box_c), debug_flags(), frames, P.nowrap ? 1 : 0,
+            0, nullptr, 0, P.d_gbar, nullptr, 0};
   alignas(64) CUtensorMap tm;
   std::memset(&tm, 0, sizeof(tm));
   if (tma) {
@@ -963,17 +986,38 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
   }
   const int threads = fwd ? (P.fwd_g == 2 ? kFwd2Threads : kFwdThreads) : (tma ? kBack4Threads : kBackThreads);
   const int stages = fwd ? kFwdStages : kBackStages;
-  const size_t smem = (size_t)stages * slot * sizeof(float) + 16 * stages;  // + full/empty mbarriers
+  // + full mbarriers (8 B per stage) and 8 B per stage + 64 B for release counters / producer state
+  const size_t smem = (size_t)stages * slot * sizeof(float) + 16 * stages + 64;
   A.frames = frames;
-  for (const Page& pg : pages) {
+  for (size_t ip = 0; ip < pages.size(); ++ip) {
+    const Page& pg = pages[ip];
     // TMA kernels are persistent (2 CTAs per SM walk the page's items); element-loader kernels are
     // one CTA per (tile, chunk, frame)
     const long long items = (long long)pg.total_items * frames;
     const int per_sm = 2;  // resident CTAs per SM (persistent TMA kernels)
     dim3 grid = tma ? dim3((unsigned)std::min<long long>(items, (long long)per_sm * P.sms), 1, 1)
                     : dim3(pg.max_tiles, pg.nchunks, frames);
+    bool coop = false;
+    A.ratio_mode = 0;
+    A.zero_count = 0;
+    if (fuse && tma) {
+      if (fwd && ip + 1 == pages.size() && fuse->ratio_mode) {
+        A.ratio_mode = fuse->ratio_mode;
+        A.meas = fuse->meas;
+        A.ratio_count = fuse->ratio_count;
+        coop = true;
+#ifdef CTIS_ZERO_IN_FWD
+        A.zero_buf = fuse->zero_buf;
+        A.zero_count = fuse->zero_count;
+#endif
+      }
+      if (!fwd && ip == 0 && fuse->zero_count) {
+        A.zero_buf = fuse->zero_buf;
+        A.zero_count = fuse->zero_count;
+      }
+    }
     void* args[] = {&A, &tm};
-    cudaError_t e = launch_pdl((const void*)pg.kern, grid, dim3(threads), args, smem, s);
+    cudaError_t e = launch_pdl((const void*)pg.kern, grid, dim3(threads), args, smem, s, coop);
     if (e != cudaSuccess) return e;
     if (count) ++*count;
   }
@@ -981,7 +1025,8 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
 }
 
 // g_hat (accumulated with red.add: must be zero on entry) += H f
-cudaError_t enqueue_forward(ctis_plan_s& P, const float* f, float* ghat, int frames, cudaStream_t s, int64_t* cnt) {
+cudaError_t enqueue_forward(ctis_plan_s& P, const float* f, float* ghat, int frames, cudaStream_t s, int64_t* cnt,
+                            const Fuse* fuse = nullptr) {
   if (P.projector == 1) {  // the paper's Fourier route (comparator arm)
     for (int z = 0; z < frames; ++z) {
       cudaError_t e = fft_forward_accumulate(P.fft, f + (size_t)z * P.m, ghat + (size_t)z * P.n, s, cnt);
@@ -989,11 +1034,11 @@ cudaError_t enqueue_forward(ctis_plan_s& P, const float* f, float* ghat, int fra
     }
     return cudaSuccess;
   }
-  return launch_pages(P, P.fwd, f, ghat, P.m, P.n, frames, 0, s, cnt);
+  return launch_pages(P, P.fwd, f, ghat, P.m, P.n, frames, 0, s, cnt, fuse);
 }
 
 cudaError_t enqueue_back(ctis_plan_s& P, const float* r, float* fz, int frames, int mode, cudaStream_t s,
-                         int64_t* cnt) {
+                         int64_t* cnt, const Fuse* fuse = nullptr) {
   if (P.projector == 1) {
     for (int z = 0; z < frames; ++z) {
       cudaError_t e = fft_back(P.fft, r + (size_t)z * P.n, fz + (size_t)z * P.m, mode, s, cnt);
@@ -1001,7 +1046,7 @@ cudaError_t enqueue_back(ctis_plan_s& P, const float* r, float* fz, int frames, 
     }
     return cudaSuccess;
   }
-  return launch_pages(P, P.back, r, fz, P.n, P.m, frames, mode, s, cnt);
+  return launch_pages(P, P.back, r, fz, P.n, P.m, frames, mode, s, cnt, fuse);
 }
 
 ctis_status validate_data(ctis_plan_s& P, const float* g, const float* f, int64_t frames, cudaStream_t s) {
@@ -1021,6 +1066,42 @@ cudaError_t enqueue_mlem(ctis_plan_s& P, const float* g, float* f, float* ws, in
   float* A = ws;
   float* B = ws + (((size_t)P.n * frames + 3) & ~(size_t)3);  // 16-byte aligned second half
   const long long count = (long long)P.n * frames;
+  if (P.fused_ratio && P.projector == 0 && P.tma_f && !P.fwd.empty()) {
+    // two kernels per iteration: forward (+ ratio in place after its grid barrier) into the current
+    // half, back (reading r there) zeroing the other half for the next iteration's forward
+    cudaError_t e = cudaMemsetAsync(A, 0, sizeof(float) * (size_t)count, s);
+    for (int k = 0; k < iters && e == cudaSuccess; ++k) {
+      float* cur = (k & 1) ? B : A;
+      float* nxt = (k & 1) ? A : B;
+      Fuse ff;
+      ff.ratio_mode = solver == 1 ? 2 : 1;
+      ff.meas = g;
+      ff.ratio_count = count;
+      const bool last = k + 1 == iters;
+#ifdef CTIS_ZERO_IN_FWD
+      if (!last) {  // nxt was r of the previous iteration's back kernel, which has completed
+        ff.zero_buf = nxt;
+        ff.zero_count = count;
+      }
+#endif
+      e = enqueue_forward(P, f, cur, frames, s, cnt, &ff);
+      if (e != cudaSuccess) break;
+      Fuse fb;
+#ifdef CTIS_ZERO_IN_FWD
+      e = enqueue_back(P, cur, f, frames, solver == 1 ? 2 : 1, s, cnt, &fb);
+      continue;
+#endif
+      if (!last && P.tma_b) {
+        fb.zero_buf = nxt;
+        fb.zero_count = count;
+      } else if (!last) {
+        e = cudaMemsetAsync(nxt, 0, sizeof(float) * (size_t)count, s);
+        if (e != cudaSuccess) break;
+      }
+      e = enqueue_back(P, cur, f, frames, solver == 1 ? 2 : 1, s, cnt, &fb);
+    }
+    return e;
+  }
   cudaError_t e = cudaMemsetAsync(A, 0, sizeof(float) * (size_t)count, s);
   for (int k = 0; k < iters && e == cudaSuccess; ++k) {
     e = enqueue_forward(P, f, A, frames, s, cnt);
@@ -1078,8 +1159,9 @@ ctis_status run_mlem(ctis_plan_s& P, const float* g, float* f, int64_t frames, i
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
     it = P.graphs.emplace(key, exec).first;
+    P.graph_launches[key] = cnt;
   } else {
-    cnt = (int64_t)iters * ((int64_t)P.fwd.size() + (int64_t)P.back.size() + 1);
+    cnt = P.graph_launches[key];
   }
   CTIS_CUDA(cudaEventRecord(P.ev_in, s), "event record");
   CTIS_CUDA(cudaStreamWaitEvent(P.side, P.ev_in, 0), "stream wait");
@@ -1381,6 +1463,13 @@ ctis_status ctis_set_option(ctis_plan p, int option, int64_t value) {
       p->projector = (int)value;
       return CTIS_OK;
     }
+    case CTIS_OPT_FUSED_RATIO:
+      if (p->fused_ratio != (value != 0)) {
+        for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+        p->graphs.clear();
+      }
+      p->fused_ratio = value != 0;
+      return CTIS_OK;
     default: return fail(CTIS_ERR_INVALID_ARGUMENT, "unknown option");
   }
 }

@@ -79,6 +79,16 @@ struct TabArgs {
   int dbg;             // profiling switches (CTIS_DEBUG env): 1 = no TMA (compute on stale windows), 2 = no flush
   int frames;          // persistent kernels: frames in the launch (items = frames x page items)
   int nowrap;          // every tap is a plain 2-D translation inside the FPA (no carry / wrap of Eq. 7)
+  // fused ratio (persistent TMA forward, last page of the projection): after a grid-wide barrier,
+  // dst[i] <- ratio(meas[i], dst[i]) for i < ratio_count (1: g / g_hat, 0 where g_hat <= 0 — Alg. 1
+  // line 8, reading R4; 2: SMART log-ratio, reading R17; 0: none)
+  int ratio_mode;
+  const float* meas;   // g
+  long long ratio_count;
+  unsigned* gbar;      // grid barrier word (zero-initialised once, self-resetting)
+  // back kernel: zero zero_count floats at zero_buf (the next iteration's g_hat accumulator)
+  float* zero_buf;
+  long long zero_count;
 };
 
 }  // namespace ctis

@@ -115,6 +115,18 @@ __device__ __forceinline__ unsigned atom_add_shared(unsigned addr, unsigned v) {
 __device__ __forceinline__ void st_shared_u32(unsigned addr, unsigned v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned ld_shared_u32(unsigned addr) {
+  unsigned v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+// slot release counter: release orders this warp's reads of the slot before the increment, acquire
+// makes every earlier release (the other warps' reads) visible to the warp that completes the count
+__device__ __forceinline__ unsigned atom_add_acqrel_shared(unsigned addr, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_3d(unsigned dst, const CUtensorMap* tm, int c0, int c1, int c2, unsigned bar) {
@@ -536,7 +548,81 @@ __device__ __forceinline__ void red_nz(float* p, float v) {
       : "memory");
 }
 
-template <int MAXM, int S, bool EARLY>
+// Grid-wide barrier for persistent launches (every CTA resident: cooperative launch).  The word is
+// zero-initialised once; CTA 0 adds 2^31 - (G - 1), the others 1, so the top bit flips exactly when
+// all G CTAs have arrived and the low bits return to their old value (self-resetting across launches).
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+    __threadfence();  // this CTA's g_hat reductions are performed before its arrival
+    const unsigned old = atomicAdd(bar, inc);
+    unsigned cur;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+      if ((old ^ cur) & 0x80000000u) break;
+      __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// r = g (/) g_hat in place over [0, count) (mode 1; reading R4) or the SMART log-ratio (mode 2; R17),
+// grid-stride with float4 (both buffers 16-byte aligned, count of any size).
+__device__ __forceinline__ float ratio_one(int mode, float g, float h) {
+  if (mode == 2) return (g > 0.f && h > 0.f) ? logf(__fdiv_rn(g, h)) : 0.f;
+  return h > 0.f ? __fdiv_rn(g, h) : 0.f;
+}
+__device__ __forceinline__ void ratio_pass(const TabArgs& A) {
+  const long long n4 = A.ratio_count >> 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const float4* g4 = reinterpret_cast<const float4*>(A.meas);
+  float4* h4 = reinterpret_cast<float4*>(A.dst);
+  // U float4 of g and g_hat in flight per thread (the persistent grid has ~4x fewer threads than a
+  // standalone element-wise launch: memory-level parallelism comes from the unroll)
+  constexpr int U = 4;
+  long long i = t0;
+  for (; i + (U - 1) * stride < n4; i += U * stride) {
+    float4 gv[U], hv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      gv[u] = __ldg(g4 + i + u * stride);
+      hv[u] = __ldcg(h4 + i + u * stride);  // L2: the reductions of every CTA landed there
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      h4[i + u * stride] = make_float4(ratio_one(A.ratio_mode, gv[u].x, hv[u].x), ratio_one(A.ratio_mode, gv[u].y, hv[u].y),
+                                       ratio_one(A.ratio_mode, gv[u].z, hv[u].z), ratio_one(A.ratio_mode, gv[u].w, hv[u].w));
+  }
+  for (; i < n4; i += stride) {
+    const float4 gv = __ldg(g4 + i);
+    const float4 hv = __ldcg(h4 + i);
+    h4[i] = make_float4(ratio_one(A.ratio_mode, gv.x, hv.x), ratio_one(A.ratio_mode, gv.y, hv.y),
+                        ratio_one(A.ratio_mode, gv.z, hv.z), ratio_one(A.ratio_mode, gv.w, hv.w));
+  }
+  for (long long i = 4 * n4 + t0; i < A.ratio_count; i += stride)
+    A.dst[i] = ratio_one(A.ratio_mode, __ldg(A.meas + i), __ldcg(A.dst + i));
+}
+
+// zero the next iteration's g_hat accumulator (back kernel prologue; nobody reads it meanwhile)
+__device__ __forceinline__ void zero_pass(const TabArgs& A) {
+  const long long n4 = A.zero_count >> 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  float4* z4 = reinterpret_cast<float4*>(A.zero_buf);
+  for (long long i = t0; i < n4; i += stride) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (long long i = 4 * n4 + t0; i < A.zero_count; i += stride) A.zero_buf[i] = 0.f;
+}
+
+#ifndef CTIS_FWD_NPRE
+#define CTIS_FWD_NPRE 0
+#endif
+#ifndef CTIS_FWD_PROBE
+#define CTIS_FWD_PROBE 1
+#endif
+template <int MAXM, int S, bool EARLY, int NPRE = CTIS_FWD_NPRE, int PROBE = CTIS_FWD_PROBE>
 __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUtensorMap* tm) {
   extern __shared__ __align__(128) float smem[];
   constexpr int K = S / 2, MP = MAXM / 2;
@@ -607,11 +693,24 @@ __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUte
     float2 a0[MP], a1[MP];
 #pragma unroll
     for (int q = 0; q < MP; ++q) a0[q] = a1[q] = make_float2(0.f, 0.f);
+    // The first NPRE tap entries of each band are loaded one band ahead: the LDS at the head of a band
+    // otherwise waits for the constant-bank load of its entry (ncu: ~25% of the samples at C4).
+    constexpr int NP = NPRE < MP ? NPRE : MP;
+    uint4 pre[NP > 0 ? NP : 1];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) pre[q] = tab4(TP)[q];
     auto compute = [&](unsigned off, int b) {
       const uint4* ent = tab4(TP) + b * MP;
+      uint4 cur[NP > 0 ? NP : 1];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) cur[q] = pre[q];
+      if (b + 1 < nb) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) pre[q] = ent[MP + q];
+      }
 #pragma unroll
       for (int q = 0; q < MP; ++q) {
-        const uint4 e = ent[q];
+        const uint4 e = q < NP ? cur[q < NP ? q : 0] : ent[q];
         const float2 wv = make_float2(__uint_as_float(e.z), __uint_as_float(e.w));
         a0[q] = __ffma2_rn(wv, make_float2(lds(tb0 + off + e.x), lds(tb0 + off + e.y)), a0[q]);
         a1[q] = __ffma2_rn(wv, make_float2(lds(tb1 + off + e.x), lds(tb1 + off + e.y)), a1[q]);
@@ -630,11 +729,13 @@ __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUte
         next_refill = w + K;
       }
       if (!(A.dbg & 1) && !ready) mbar_wait(full + 8 * c_slot, c_phase);
-      // probe the next window's barrier now: its latency overlaps this band's tap loop, and the next
-      // trip skips the blocking wait when the window had already landed
       const unsigned n_slot = c_slot + 1 == S ? 0u : c_slot + 1, n_phase = c_slot + 1 == S ? c_phase ^ 1u : c_phase;
-      const bool ready_next = EARLY && mbar_test(full + 8 * n_slot, n_phase);
+      // PROBE 1: probe the next window's barrier before the tap loop; PROBE 2: after it (the probe has
+      // acquire semantics, so shared loads issued after it wait for it); PROBE 0: plain waits only
+      bool ready_next = false;
+      if (EARLY && PROBE == 1) ready_next = mbar_test(full + 8 * n_slot, n_phase);
       compute(c_slot * slot_bytes, b);
+      if (EARLY && PROBE == 2) ready_next = mbar_test(full + 8 * n_slot, n_phase);
       c_slot = n_slot;
       c_phase = n_phase;
       ready = ready_next;
@@ -681,6 +782,13 @@ __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUte
       }
     }
   }
+  if (A.ratio_mode) {  // fused ratio (Alg. 1 line 8) once every CTA's reductions have landed
+    grid_sync(A.gbar);
+    ratio_pass(A);
+#ifdef CTIS_ZERO_IN_FWD
+    if (A.zero_count) zero_pass(A);
+#endif
+  }
 }
 
 // Programmatic dependent launch: let the next kernel of the MLEM chain be scheduled as soon as this
@@ -703,7 +811,13 @@ __device__ __forceinline__ void nan_fill_smem(int nf) {
 // entry read through the uniform datapath feeds eight shared-memory loads (cf. forward_persistent2).
 // POS voxels per thread: columns warp + 8k (k < POS) of a 32 x 8*POS tile (POS = 2 for small problems,
 // where 32 x 32 tiles would leave SMs idle)
-template <int NB, int POS>
+#ifndef CTIS_BACK_NPRE
+#define CTIS_BACK_NPRE 0
+#endif
+#ifndef CTIS_BACK_REFILL
+#define CTIS_BACK_REFILL 0
+#endif
+template <int NB, int POS, int NPRE = CTIS_BACK_NPRE, bool REFILL = CTIS_BACK_REFILL>
 __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtensorMap* tm) {
   constexpr int TC = 8 * POS;
   extern __shared__ __align__(128) float smem[];
@@ -712,6 +826,9 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
   const int nch = tabi(0);
   const int per_frame = tabi(kItemBase + nch);
   const int items = per_frame * A.frames;
+#ifndef CTIS_ZERO_AT_END
+  if (A.zero_count) zero_pass(A);
+#endif
   if ((int)blockIdx.x >= items) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
@@ -756,14 +873,56 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
       if (p_item < items) p_load_item();
     }
   };
+  // REFILL: window w + S is loaded into slot w % S by the last warp to finish window w (release
+  // counters cnt[S], producer state in shared memory); no CTA-wide refill barrier
+  const unsigned cnt = full + 8 * S, pst = cnt + 4 * S;
+  auto save_state = [&]() {
+    st_shared_u32(pst + 0, (unsigned)p_item);
+    st_shared_u32(pst + 4, (unsigned)p_mode);
+    st_shared_u32(pst + 8, (unsigned)p_nm);
+    st_shared_u32(pst + 12, (unsigned)p_z);
+    st_shared_u32(pst + 16, (unsigned)p_qr);
+    st_shared_u32(pst + 20, (unsigned)p_qc);
+    st_shared_u32(pst + 24, p_MI);
+    st_shared_u32(pst + 28, p_w);
+  };
+  auto load_state = [&]() {
+    p_item = (int)ld_shared_u32(pst + 0);
+    p_mode = (int)ld_shared_u32(pst + 4);
+    p_nm = (int)ld_shared_u32(pst + 8);
+    p_z = (int)ld_shared_u32(pst + 12);
+    p_qr = (int)ld_shared_u32(pst + 16);
+    p_qc = (int)ld_shared_u32(pst + 20);
+    p_MI = ld_shared_u32(pst + 24);
+    p_w = ld_shared_u32(pst + 28);
+  };
   if (threadIdx.x == 0) {
     for (int q = 0; q < S; ++q) mbar_init(full + 8 * q, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     p_load_item();
 #pragma unroll
     for (int q = 0; q < S; ++q) issue_one();
+    if (REFILL) {
+      for (int q = 0; q < S; ++q) st_shared_u32(cnt + 4 * q, 0u);
+      save_state();
+    }
   }
   __syncthreads();
+  // after consuming window wi: the warp that completes slot wi % S's count issues window wi + S
+  auto release = [&](unsigned wi) {
+    __syncwarp();
+    if (lane == 0) {
+      const unsigned old = atom_add_acqrel_shared(cnt + 4 * (wi & (S - 1)), 1u);
+      if (old % NWARPS == NWARPS - 1) {
+        fence_proxy_async();
+        load_state();
+        if (p_item < items) {
+          issue_one();
+          save_state();
+        }
+      }
+    }
+  };
 
   const unsigned t0 = sbase + 4u * (lane + A.box_r * warp), cstep = 4u * A.box_r * NWARPS;
   unsigned w = 0, next_refill = K;
@@ -779,11 +938,23 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
     for (int k4 = 0; k4 < POS; ++k4)
 #pragma unroll
       for (int q = 0; q < BP; ++q) acc[k4][q] = make_float2(0.f, 0.f);
+    // first NPRE entries of each mode loaded one mode ahead (see forward_persistent2)
+    constexpr int NP = NPRE < BP ? NPRE : BP;
+    uint4 pre[NP > 0 ? NP : 1];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) pre[q] = tab4(TP)[q];
     auto compute = [&](unsigned ba, int c) {
       const uint4* ent = tab4(TP) + c * BP;
+      uint4 cur[NP > 0 ? NP : 1];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) cur[q] = pre[q];
+      if (c + 1 < nm) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) pre[q] = ent[BP + q];
+      }
 #pragma unroll
       for (int q = 0; q < BP; ++q) {
-        const uint4 e = ent[q];
+        const uint4 e = q < NP ? cur[q < NP ? q : 0] : ent[q];
         const float2 wv = make_float2(__uint_as_float(e.z), __uint_as_float(e.w));
 #pragma unroll
         for (int k4 = 0; k4 < POS; ++k4) {
@@ -793,7 +964,7 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
       }
     };
     for (int c = 0; c < nm;) {
-      if (w >= next_refill) {
+      if (!REFILL && w >= next_refill) {
         __syncthreads();
         if (threadIdx.x == 0) {
 #pragma unroll 1
@@ -805,10 +976,12 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
       const unsigned s0 = w & (S - 1);
       mbar_wait(full + 8 * s0, (w / S) & 1u);
       compute(t0 + s0 * slot_bytes, c);
+      if (REFILL) release(w);
       if (c + 1 < nm) {
         const unsigned s1 = (w + 1) & (S - 1);
         mbar_wait(full + 8 * s1, ((w + 1) / S) & 1u);
         compute(t0 + s1 * slot_bytes, c + 1);
+        if (REFILL) release(w + 1);
         w += 2;
         c += 2;
       } else {
@@ -855,6 +1028,9 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
       }
     }
   }
+#ifdef CTIS_ZERO_AT_END
+  if (A.zero_count) zero_pass(A);  // CTAs that finish early fill the tail with the zeroing
+#endif
 }
 
 }  // namespace

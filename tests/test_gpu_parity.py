@@ -292,6 +292,33 @@ def test_band_shards_wrapping_taps_vs_oracle(ctis, oracle_lib, dev, nshards):
     check(torch.cat(out).cpu().numpy(), want, MLEM_TOL, f"wrapping band-sharded MLEM ({nshards} shards)")
 
 
+# ------------------------------------------------------------------ fused ratio (CTIS_OPT_FUSED_RATIO = 1)
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_fused_ratio_option_vs_oracle(ctis, oracle_lib, dev, name):
+    """Two kernels per iteration: the cooperative forward turns g_hat into r after a grid barrier, the
+    back kernel zeroes the other workspace half.  MLEM (single and batched) and SMART vs the oracle."""
+    cfg = syn.config(name)
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    plan.set_option(ctis.OPT_FUSED_RATIO, 1)
+    g_np = oracle_lib.forward(geom, taps, syn.scene_blobs(geom)).astype(np.float32)
+    g = cuda(g_np, dev)
+    f = torch.ones(geom.m, device=dev)
+    plan.mlem(g, f, 30)
+    assert plan.last_launch_count() == 30 * (plan.info()["fwd_pages"] + plan.info()["back_pages"])
+    check(f.cpu().numpy(), oracle_lib.mlem(geom, taps, g_np, np.ones(geom.m), 30), MLEM_TOL, f"{name} fused MLEM K=30")
+    fs = torch.ones(geom.m, device=dev)
+    plan.smart(g, fs, 10)
+    check(fs.cpu().numpy(), oracle_lib.smart(geom, taps, g_np, np.ones(geom.m), 10), MLEM_TOL, f"{name} fused SMART")
+    F = 3
+    gb = torch.stack([g, g * 0.5, g * 2.0]).contiguous()
+    fb = torch.ones(F, geom.m, device=dev)
+    plan.mlem(gb, fb, 12)
+    for i, sc in enumerate((1.0, 0.5, 2.0)):
+        want = oracle_lib.mlem(geom, taps, g_np.astype(np.float64) * sc, np.ones(geom.m), 12)
+        check(fb[i].cpu().numpy(), want, MLEM_TOL, f"{name} fused batched frame {i}")
+
+
 # ------------------------------------------------------------------ latency mode through libctis + NCCL
 @pytest.mark.parametrize("case", ["C2", "C3", "wrap"])
 def test_band_sharded_nccl_single_rank_vs_oracle(ctis, oracle_lib, dev, case):

@@ -14,6 +14,8 @@ solver = sys.argv[3] if len(sys.argv) > 3 else "mlem"   # mlem | monitored | sma
 cfg = syn.config(name)
 plan = ctis.Plan.from_geometry(cfg.geom, syn.paper_taps(cfg))
 plan.set_option(ctis.OPT_VALIDATE_DATA, 0)
+if os.environ.get("CTIS_FUSED") == "0":
+    plan.set_option(ctis.OPT_FUSED_RATIO, 0)
 g = plan.forward(torch.from_numpy(syn.scene_blobs(cfg.geom).reshape(-1)).cuda())
 f = torch.ones(cfg.geom.m, device="cuda")
 def run():
@@ -37,4 +39,4 @@ for _ in range(15):
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b) * 1e3 / K)
 ts.sort()
-print(f"{name} {solver} pdl={os.environ.get('CTIS_PDL', '0')} us/iter min {ts[0]:.1f} med {ts[len(ts) // 2]:.1f} max {ts[-1]:.1f}")
+print(f"{name} {solver} pdl={os.environ.get('CTIS_PDL', '0')} fused={os.environ.get('CTIS_FUSED', '1')} launches={plan.last_launch_count()} us/iter min {ts[0]:.1f} med {ts[len(ts) // 2]:.1f} max {ts[-1]:.1f}")
