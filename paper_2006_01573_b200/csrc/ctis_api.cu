@@ -135,10 +135,17 @@ struct ctis_plan_s {
   std::vector<float> inv_h;          // 1 / h_lambda per local band
   int64_t last_launches = 0;
   bool fused_ratio = false;    // CTIS_OPT_FUSED_RATIO (measured slower: DESIGN.md)
+  // Throughput layout for many-frame launches: the single-frame layout shortens forward chunks and back
+  // band chunks until one frame fills the SMs; with enough frames the longer chunks (fewer flushes, NB = 12
+  // bands per r window) win.  A second plan over the same taps, used by batched calls (nullptr if the
+  // layouts coincide).
+  bool throughput = false;     // this plan IS a throughput layout
+  ctis_plan_s* tput = nullptr;
   unsigned* d_gbar = nullptr;  // grid barrier word of the cooperative forward launches
   std::mutex mu;
 
   ~ctis_plan_s() {
+    delete tput;
     DeviceGuard dg(device);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : mon_graphs) cudaGraphExecDestroy(kv.second);
@@ -501,6 +508,18 @@ int choose_back_nb(const ctis_plan_s& P) {
     const int v = std::atoi(e);
     if (v == 2 || v == 4 || v == 8 || v == 12 || v == 16) return v;
   }
+  if (P.throughput) {  // many frames fill the SMs anyway: minimise chunks x (NB + window cost), NB <= 12
+    int best = 12;
+    long long bestc = LLONG_MAX;
+    for (int NB : {12, 8, 4, 2}) {
+      const long long c = (long long)((P.w + NB - 1) / NB) * (NB + 5);
+      if (c < bestc) {
+        bestc = c;
+        best = NB;
+      }
+    }
+    return best;
+  }
   const long long tiles = (long long)((P.a + kBackTR - 1) / kBackTR) * ((P.alpha + P.back_tc - 1) / P.back_tc);
   const long long slots = 148LL * 2;
   int best = kBackBandsMax;
@@ -544,7 +563,8 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
       const long long tiles = (long long)((P.a + 2 * fspan + kFwdTR - 1) / kFwdTR) *
                               ((P.alpha + 2 * fspan + kFwdTC - 1) / kFwdTC);
       const long long passes = ((long long)tmax + 31) / 32;
-      while (fbands > 1 && tiles * passes * ((P.w + fbands - 1) / fbands) < 2LL * P.sms) fbands = fbands / 2;
+      while (!P.throughput && fbands > 1 && tiles * passes * ((P.w + fbands - 1) / fbands) < 2LL * P.sms)
+        fbands = fbands / 2;
       if (const char* e = std::getenv("CTIS_FWD_BANDS")) fbands = std::max(1, std::atoi(e));
       if (const char* e = std::getenv("CTIS_FWD_SPAN")) fspan = std::max(1, std::min(kModeSpanMax, std::atoi(e)));
     }
@@ -625,7 +645,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
     bool allow16 = true;
   back_layout:
     P.back_nb = choose_back_nb(P);
-    if (allow16) {  // small TMA plans: 32 x 16 tiles (two voxels per thread) when 32 x 32 tiles leave CTA slots idle
+    if (allow16 && !P.throughput) {  // small TMA plans: 32 x 16 tiles (two voxels per thread) when 32 x 32 tiles leave CTA slots idle
       const long long t32 = (long long)((P.a + kBackTR - 1) / kBackTR) * ((P.alpha + kBackTC - 1) / kBackTC);
       const char* e = std::getenv("CTIS_BACK_TC");
       // measured: tiny 14.8 -> 13.3 us, C2 unchanged, C3 (208 items) 25.0 -> 25.2 us: only below one item per SM
@@ -728,7 +748,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
 
 ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64_t xi, const int64_t* tap_ptr,
                        const int64_t* tap_offset, const float* tap_weight, int64_t b0, int64_t b1, bool shard,
-                       int device, ctis_plan* out) {
+                       int device, ctis_plan* out, bool throughput = false) {
   if (!out) return fail(CTIS_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if (!tap_ptr || !tap_offset || !tap_weight) return fail(CTIS_ERR_INVALID_ARGUMENT, "tap array is NULL");
@@ -820,6 +840,7 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
     p->total_taps += (int64_t)bt.size();
   }
   p->inv_h = invh;
+  p->throughput = throughput;
   ctis_status st = build_tables(*p, bands, invh);
   cudaError_t e = cudaSuccess;
   if (!st) {
@@ -846,9 +867,39 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
     delete p;
     return cuda_fail(e, "plan upload");
   }
+  if (!throughput && !shard && p->tma_f && !std::getenv("CTIS_NO_TPUT")) {
+    ctis_plan tp = nullptr;
+    ctis_status ts = build_plan(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, b0, b1, shard, device, &tp, true);
+    if (ts) {
+      delete p;
+      return ts;
+    }
+    size_t fc = 0, tfc = 0;
+    for (const Page& pg : p->fwd) fc += pg.nchunks;
+    for (const Page& pg : tp->fwd) tfc += pg.nchunks;
+    if (fc == tfc && p->back_nb == tp->back_nb && p->back_tc == tp->back_tc && p->tma_b == tp->tma_b)
+      delete tp;  // same layout: nothing to gain
+    else
+      p->tput = tp;
+  }
   *out = p;
   g_last_error.clear();
   return CTIS_OK;
+}
+
+// Batched calls switch to the throughput layout once the frames give both projections >= 2 work items
+// per CTA slot (2 CTAs per SM) in that layout.
+ctis_plan_s* layout_for(ctis_plan_s& P, int64_t frames) {
+  if (!P.tput || frames < 2 || P.projector != 0) return &P;
+  long long fi = 0, bi = 0;
+  for (const Page& pg : P.tput->fwd) fi += pg.total_items;
+  for (const Page& pg : P.tput->back) bi += pg.total_items;
+  if ((long long)frames * std::min(fi, bi) < 4LL * P.sms) return &P;
+  ctis_plan_s* T = P.tput;
+  T->validate = P.validate;
+  T->use_graph = P.use_graph;
+  T->fused_ratio = P.fused_ratio;
+  return T;
 }
 
 bool aligned16(const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15u) == 0; }
@@ -873,6 +924,14 @@ bool pdl_enabled() {
   static bool v = [] {
     const char* e = std::getenv("CTIS_PDL");
     return e && std::atoi(e) == 1;
+  }();
+  return v;
+}
+
+int debug_flags() {
+  static int v = [] {
+    const char* e = std::getenv("CTIS_DEBUG");
+    return e ? std::atoi(e) : 0;
   }();
   return v;
 }
@@ -902,7 +961,10 @@ cudaError_t make_tensor_map(CUtensorMap* tm, bool forward, const ctis_plan_s& P,
   if (forward) {
     const cuuint64_t dims[4] = {(cuuint64_t)P.a, (cuuint64_t)P.alpha, (cuuint64_t)P.w, (cuuint64_t)frames};
     const cuuint64_t strides[3] = {4ull * P.a, 4ull * P.ell, 4ull * P.m};
-    const cuuint32_t box[4] = {(cuuint32_t)P.fbox_r, (cuuint32_t)P.fbox_c, 1u, 1u};
+    // CTIS_DEBUG & 32 (profiling only, results invalid): half-width boxes, to measure what smaller
+    // per-band windows would save in TMA traffic
+    const cuuint32_t bc = (debug_flags() & 32) ? (cuuint32_t)std::max(1, P.fbox_c / 2) : (cuuint32_t)P.fbox_c;
+    const cuuint32_t box[4] = {(cuuint32_t)P.fbox_r, bc, 1u, 1u};
     const cuuint32_t es[4] = {1u, 1u, 1u, 1u};
     r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, es,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -910,7 +972,8 @@ cudaError_t make_tensor_map(CUtensorMap* tm, bool forward, const ctis_plan_s& P,
   } else {
     const cuuint64_t dims[3] = {(cuuint64_t)P.gamma, (cuuint64_t)P.xi, (cuuint64_t)frames};
     const cuuint64_t strides[2] = {4ull * P.gamma, 4ull * P.n};
-    const cuuint32_t box[3] = {(cuuint32_t)P.bbox_r, (cuuint32_t)P.bbox_c, 1u};
+    const cuuint32_t bc = (debug_flags() & 32) ? (cuuint32_t)std::max(1, P.bbox_c / 2) : (cuuint32_t)P.bbox_c;
+    const cuuint32_t box[3] = {(cuuint32_t)P.bbox_r, bc, 1u};
     const cuuint32_t es[3] = {1u, 1u, 1u};
     r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -952,13 +1015,6 @@ struct Fuse {
   long long zero_count = 0;
 };
 
-int debug_flags() {
-  static int v = [] {
-    const char* e = std::getenv("CTIS_DEBUG");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
 
 cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const float* src, float* dst,
                          long long src_frame, long long dst_frame, int frames, int mode, cudaStream_t s,
@@ -976,7 +1032,8 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
   const int cap = fwd ? kFwdWinFloats : kBackWinFloats;
   int slot = tma ? (box_r * box_c + 31) / 32 * 32 : cap;
   TabArgs A{src, dst, src_frame, dst_frame, P.a, P.alpha, P.gamma, P.xi, P.n, P.ell, mode, bias, nsub,
-            slot, box_r, box_c, (unsigned)(4 * box_r * box_c), debug_flags(), frames, P.nowrap ? 1 : 0,
+            slot, box_r, box_c, (unsigned)(4 * box_r * ((debug_flags() & 32) ? std::max(1, box_c / 2) : box_c)),
+            debug_flags(), frames, P.nowrap ? 1 : 0,
             0, nullptr, 0, P.d_gbar, nullptr, 0};
   alignas(64) CUtensorMap tm;
   std::memset(&tm, 0, sizeof(tm));
@@ -1117,6 +1174,11 @@ cudaError_t enqueue_mlem(ctis_plan_s& P, const float* g, float* f, float* ws, in
 
 ctis_status run_mlem(ctis_plan_s& P, const float* g, float* f, int64_t frames, int iters, void* ws, cudaStream_t s,
                      int solver = 0) {
+  if (ctis_plan_s* T = layout_for(P, frames); T != &P) {
+    ctis_status st = run_mlem(*T, g, f, frames, iters, ws, s, solver);
+    P.last_launches = T->last_launches;
+    return st;
+  }
   if (P.shard)
     return fail(CTIS_ERR_INVALID_ARGUMENT,
                 "mlem on a shard plan needs the collective: use ctis_forward + all-reduce + ctis_back_update_from_ghat");
@@ -1487,9 +1549,10 @@ ctis_status ctis_forward_batched(ctis_plan p, const float* f, float* g_hat, int6
   std::lock_guard<std::mutex> lk(p->mu);
   DeviceGuard dg(p->device);
   cudaStream_t s = (cudaStream_t)stream;
+  ctis_plan_s& Q = *layout_for(*p, frames);
   p->last_launches = 0;
   CTIS_CUDA(cudaMemsetAsync(g_hat, 0, sizeof(float) * (size_t)p->n * frames, s), "forward memset");
-  CTIS_CUDA(enqueue_forward(*p, f, g_hat, (int)frames, s, &p->last_launches), "forward");
+  CTIS_CUDA(enqueue_forward(Q, f, g_hat, (int)frames, s, &p->last_launches), "forward");
   return CTIS_OK;
 }
 
@@ -1501,7 +1564,8 @@ ctis_status ctis_forward_accumulate(ctis_plan p, const float* f, float* g_hat, i
   std::lock_guard<std::mutex> lk(p->mu);
   DeviceGuard dg(p->device);
   p->last_launches = 0;
-  CTIS_CUDA(enqueue_forward(*p, f, g_hat, (int)frames, (cudaStream_t)stream, &p->last_launches), "forward");
+  CTIS_CUDA(enqueue_forward(*layout_for(*p, frames), f, g_hat, (int)frames, (cudaStream_t)stream, &p->last_launches),
+            "forward");
   return CTIS_OK;
 }
 

@@ -616,13 +616,10 @@ __device__ __forceinline__ void zero_pass(const TabArgs& A) {
   for (long long i = 4 * n4 + t0; i < A.zero_count; i += stride) A.zero_buf[i] = 0.f;
 }
 
-#ifndef CTIS_FWD_NPRE
-#define CTIS_FWD_NPRE 0
-#endif
 #ifndef CTIS_FWD_PROBE
 #define CTIS_FWD_PROBE 1
 #endif
-template <int MAXM, int S, bool EARLY, int NPRE = CTIS_FWD_NPRE, int PROBE = CTIS_FWD_PROBE>
+template <int MAXM, int S, bool EARLY, int PROBE = CTIS_FWD_PROBE>
 __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUtensorMap* tm) {
   extern __shared__ __align__(128) float smem[];
   constexpr int K = S / 2, MP = MAXM / 2;
@@ -693,24 +690,11 @@ __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUte
     float2 a0[MP], a1[MP];
 #pragma unroll
     for (int q = 0; q < MP; ++q) a0[q] = a1[q] = make_float2(0.f, 0.f);
-    // The first NPRE tap entries of each band are loaded one band ahead: the LDS at the head of a band
-    // otherwise waits for the constant-bank load of its entry (ncu: ~25% of the samples at C4).
-    constexpr int NP = NPRE < MP ? NPRE : MP;
-    uint4 pre[NP > 0 ? NP : 1];
-#pragma unroll
-    for (int q = 0; q < NP; ++q) pre[q] = tab4(TP)[q];
     auto compute = [&](unsigned off, int b) {
       const uint4* ent = tab4(TP) + b * MP;
-      uint4 cur[NP > 0 ? NP : 1];
-#pragma unroll
-      for (int q = 0; q < NP; ++q) cur[q] = pre[q];
-      if (b + 1 < nb) {
-#pragma unroll
-        for (int q = 0; q < NP; ++q) pre[q] = ent[MP + q];
-      }
 #pragma unroll
       for (int q = 0; q < MP; ++q) {
-        const uint4 e = q < NP ? cur[q < NP ? q : 0] : ent[q];
+        const uint4 e = ent[q];
         const float2 wv = make_float2(__uint_as_float(e.z), __uint_as_float(e.w));
         a0[q] = __ffma2_rn(wv, make_float2(lds(tb0 + off + e.x), lds(tb0 + off + e.y)), a0[q]);
         a1[q] = __ffma2_rn(wv, make_float2(lds(tb1 + off + e.x), lds(tb1 + off + e.y)), a1[q]);
@@ -811,13 +795,10 @@ __device__ __forceinline__ void nan_fill_smem(int nf) {
 // entry read through the uniform datapath feeds eight shared-memory loads (cf. forward_persistent2).
 // POS voxels per thread: columns warp + 8k (k < POS) of a 32 x 8*POS tile (POS = 2 for small problems,
 // where 32 x 32 tiles would leave SMs idle)
-#ifndef CTIS_BACK_NPRE
-#define CTIS_BACK_NPRE 0
-#endif
 #ifndef CTIS_BACK_REFILL
 #define CTIS_BACK_REFILL 0
 #endif
-template <int NB, int POS, int NPRE = CTIS_BACK_NPRE, bool REFILL = CTIS_BACK_REFILL>
+template <int NB, int POS, bool REFILL = CTIS_BACK_REFILL>
 __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtensorMap* tm) {
   constexpr int TC = 8 * POS;
   extern __shared__ __align__(128) float smem[];
@@ -938,23 +919,11 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
     for (int k4 = 0; k4 < POS; ++k4)
 #pragma unroll
       for (int q = 0; q < BP; ++q) acc[k4][q] = make_float2(0.f, 0.f);
-    // first NPRE entries of each mode loaded one mode ahead (see forward_persistent2)
-    constexpr int NP = NPRE < BP ? NPRE : BP;
-    uint4 pre[NP > 0 ? NP : 1];
-#pragma unroll
-    for (int q = 0; q < NP; ++q) pre[q] = tab4(TP)[q];
     auto compute = [&](unsigned ba, int c) {
       const uint4* ent = tab4(TP) + c * BP;
-      uint4 cur[NP > 0 ? NP : 1];
-#pragma unroll
-      for (int q = 0; q < NP; ++q) cur[q] = pre[q];
-      if (c + 1 < nm) {
-#pragma unroll
-        for (int q = 0; q < NP; ++q) pre[q] = ent[BP + q];
-      }
 #pragma unroll
       for (int q = 0; q < BP; ++q) {
-        const uint4 e = q < NP ? cur[q < NP ? q : 0] : ent[q];
+        const uint4 e = ent[q];
         const float2 wv = make_float2(__uint_as_float(e.z), __uint_as_float(e.w));
 #pragma unroll
         for (int k4 = 0; k4 < POS; ++k4) {

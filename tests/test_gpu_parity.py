@@ -305,7 +305,7 @@ def test_fused_ratio_option_vs_oracle(ctis, oracle_lib, dev, name):
     g = cuda(g_np, dev)
     f = torch.ones(geom.m, device=dev)
     plan.mlem(g, f, 30)
-    assert plan.last_launch_count() == 30 * (plan.info()["fwd_pages"] + plan.info()["back_pages"])
+    assert plan.last_launch_count() == 2 + 30 * (plan.info()["fwd_pages"] + plan.info()["back_pages"])  # + validation
     check(f.cpu().numpy(), oracle_lib.mlem(geom, taps, g_np, np.ones(geom.m), 30), MLEM_TOL, f"{name} fused MLEM K=30")
     fs = torch.ones(geom.m, device=dev)
     plan.smart(g, fs, 10)
