@@ -9,7 +9,7 @@ LIBOUT   ?= $(PKG)/libctis.so
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden \
             --expt-relaxed-constexpr -Iinclude $(EXTRA)
 HDRS     := include/ctis.h $(PKG)/csrc/ctis_internal.h $(PKG)/csrc/ctis_kernels.h $(PKG)/csrc/ctis_fft.h \
-            $(PKG)/csrc/ctis_comm.h
+            $(PKG)/csrc/ctis_comm.h $(PKG)/csrc/ctis_nvls.h
 # nccl.h for the latency mode's types (the library itself is dlopen'ed at run time)
 NCCL_INC ?= $(shell python -c "import os, nvidia.nccl as m; print(os.path.join(list(m.__path__)[0], 'include'))" 2>/dev/null || echo /usr/include)
 
@@ -34,6 +34,11 @@ $(BUILD)/ctis_comm.o: $(PKG)/csrc/ctis_comm.cu $(HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -I$(NCCL_INC) -c $< -o $@
 
+# the fused NVLink exchange kernel uses NCCL's device API (header-only device code, nccl_device.h)
+$(BUILD)/ctis_nvls.o: $(PKG)/csrc/ctis_nvls.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -I$(NCCL_INC) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ctis_nvls.ptxas.log || (cat $(BUILD)/ctis_nvls.ptxas.log; false)
+
 $(BUILD)/ctis_fft.o: $(PKG)/csrc/ctis_fft.cu $(HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
@@ -42,7 +47,8 @@ $(BUILD)/ctis_kernels.o: $(PKG)/csrc/ctis_kernels.cu $(HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ctis_kernels.ptxas.log || (cat $(BUILD)/ctis_kernels.ptxas.log; false)
 
-$(LIBOUT): $(BUILD)/ctis_api.o $(BUILD)/ctis_kernels.o $(BUILD)/ctis_fft.o $(BUILD)/ctis_comm.o $(BUILD)/ctis_tables_blob.o
+$(LIBOUT): $(BUILD)/ctis_api.o $(BUILD)/ctis_kernels.o $(BUILD)/ctis_fft.o $(BUILD)/ctis_comm.o $(BUILD)/ctis_nvls.o \
+          $(BUILD)/ctis_tables_blob.o
 	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC -o $@.tmp $^ -lcufft -ldl && mv $@.tmp $@
 
 oracle/liboracle.so: oracle/ctis_oracle.c

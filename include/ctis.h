@@ -84,13 +84,21 @@ typedef enum {
                                    plan — a comparator arm.  Allocates O(w n) complex
                                    scratch owned by the plan (CTIS_ERR_OUT_OF_MEMORY if it does not fit):
                                    calls on one plan must then not run concurrently on different streams. */
-  CTIS_OPT_FUSED_RATIO = 4      /* 1: ctis_mlem / ctis_mlem_batched / ctis_smart on plans with
+  CTIS_OPT_FUSED_RATIO = 4,     /* 1: ctis_mlem / ctis_mlem_batched / ctis_smart on plans with
                                    persistent (TMA) forward kernels run two kernels per iteration: the
                                    forward's last launch is cooperative and, after a grid-wide barrier,
                                    turns g_hat into r = g (/) g_hat in place (Alg. 1 line 8); the back
                                    kernel zeroes the other workspace half for the next forward.
                                    0 (default): three kernels per iteration (separate ratio pass),
                                    measured faster on B200 (C4 149.5 vs 150.8 us per iteration). */
+  CTIS_OPT_EXCHANGE = 5         /* latency mode (ctis_mlem_band_sharded) exchange: 0 (default) NCCL
+                                   reduce-scatter + ratio kernel + all-gather; 1 ONE fused kernel over
+                                   NVLink peer memory: the exchange buffer is an NCCL
+                                   symmetric-memory window owned by the communicator, each rank reduces
+                                   its pixel slice across all ranks (multimem.ld_reduce over NVSwitch when
+                                   NVLS is available, else peer loads), forms r = g (/) g_hat and stores it
+                                   to every rank (multimem.st / peer stores).  Needs NCCL >= 2.28; the
+                                   `ws` argument is then unused. */
 } ctis_option;
 
 /* Create a plan for the full operator H (all w bands).

@@ -68,7 +68,7 @@ EXPORTED = tuple(_SIGS)
 # status codes (include/ctis.h)
 OK, ERR_INVALID_ARGUMENT, ERR_DIMENSION, ERR_TAP, ERR_ZERO_SENSITIVITY, ERR_DATA, ERR_CUDA, \
     ERR_OUT_OF_MEMORY, ERR_UNSUPPORTED = range(9)
-OPT_VALIDATE_DATA, OPT_USE_GRAPH, OPT_PROJECTOR, OPT_FUSED_RATIO = 1, 2, 3, 4
+OPT_VALIDATE_DATA, OPT_USE_GRAPH, OPT_PROJECTOR, OPT_FUSED_RATIO, OPT_EXCHANGE = 1, 2, 3, 4, 5
 
 
 def comm_unique_id() -> bytes:

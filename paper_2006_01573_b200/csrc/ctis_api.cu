@@ -17,6 +17,7 @@
 
 #include "../../include/ctis.h"
 #include "ctis_comm.h"
+#include "ctis_nvls.h"
 #include "ctis_internal.h"
 #include "ctis_fft.h"
 #include "ctis_kernels.h"
@@ -135,6 +136,7 @@ struct ctis_plan_s {
   std::vector<float> inv_h;          // 1 / h_lambda per local band
   int64_t last_launches = 0;
   bool fused_ratio = false;    // CTIS_OPT_FUSED_RATIO (measured slower: DESIGN.md)
+  int exchange = 0;            // CTIS_OPT_EXCHANGE: 0 NCCL collectives, 1 fused NVLink kernel
   // Throughput layout for many-frame launches: the single-frame layout shortens forward chunks and back
   // band chunks until one frame fills the SMs; with enough frames the longer chunks (fewer flushes, NB = 12
   // bands per r window) win.  A second plan over the same taps, used by batched calls (nullptr if the
@@ -165,7 +167,11 @@ struct ctis_plan_s {
 struct ctis_comm_s {
   void* nccl = nullptr;
   int nranks = 1, rank = 0, device = 0;
-  ~ctis_comm_s() { ctis::nccl_comm_destroy(nccl); }
+  ctis::NvlsComm nvls;  // symmetric exchange window + device communicator (CTIS_OPT_EXCHANGE = 1)
+  ~ctis_comm_s() {
+    ctis::nvls_teardown(nccl, &nvls);
+    ctis::nccl_comm_destroy(nccl);
+  }
 };
 
 namespace {
@@ -1361,6 +1367,12 @@ ctis_status enqueue_band_sharded(ctis_plan_s& P, ctis_comm_s& C, const float* g,
   for (int k = 0; k < iters; ++k) {
     if (k > 0) CTIS_CUDA(cudaMemsetAsync(X + ex.base, 0, sizeof(float) * (size_t)(ex.slice * C.nranks), s), "memset");
     CTIS_CUDA(enqueue_forward(P, f, X, 1, s, cnt), "partial forward");
+    if (P.exchange == 1) {  // f-1: reduce my slice over all ranks, ratio, store r to every rank: one kernel
+      CTIS_CUDA(launch_exchange_ratio(C.nvls, ex.base, ex.slice, g, P.n, s), "fused exchange + ratio");
+      ++*cnt;
+      CTIS_CUDA(enqueue_back(P, X, f, 1, 1, s, cnt), "back update");
+      continue;
+    }
     if (!nccl_reduce_scatter_f32(X + ex.base, slice, (size_t)ex.slice, C.nccl, s, &err)) return fail(CTIS_ERR_CUDA, err);
     if (ratio_count > 0) {
       CTIS_CUDA(launch_ratio(g + s0, slice, slice, ratio_count, false, s), "slice ratio");
@@ -1382,9 +1394,20 @@ ctis_status run_band_sharded(ctis_plan_s& P, ctis_comm_s& C, const float* g, flo
   P.last_launches = 0;
   if (iters == 0) return CTIS_OK;
   float* X = static_cast<float*>(ws);
+  if (P.exchange == 1) {  // the exchange buffer is the communicator's symmetric window (collective setup)
+    const size_t need = sizeof(float) * (size_t)exchange_layout(P, C).floats;
+    if (C.nvls.bytes < need) {
+      nvls_teardown(C.nccl, &C.nvls);
+      std::string err;
+      if (!nvls_setup(C.nccl, need, C.device, &C.nvls, &err)) return fail(CTIS_ERR_UNSUPPORTED, err);
+      for (auto& kv : P.shard_graphs) cudaGraphExecDestroy(kv.second);
+      P.shard_graphs.clear();
+    }
+    X = static_cast<float*>(C.nvls.buf);
+  }
   int64_t cnt = 0;
   if (!P.use_graph) return enqueue_band_sharded(P, C, g, f, X, iters, s, &P.last_launches);
-  GraphKey key{g, f, ws, (int64_t)reinterpret_cast<intptr_t>(&C), iters, 2};
+  GraphKey key{g, f, X, (int64_t)reinterpret_cast<intptr_t>(&C), iters, 2 + P.exchange};
   auto it = P.shard_graphs.find(key);
   if (it == P.shard_graphs.end()) {
     if (P.shard_graphs.size() >= 8) {
@@ -1525,6 +1548,10 @@ ctis_status ctis_set_option(ctis_plan p, int option, int64_t value) {
       p->projector = (int)value;
       return CTIS_OK;
     }
+    case CTIS_OPT_EXCHANGE:
+      if (value != 0 && value != 1) return fail(CTIS_ERR_INVALID_ARGUMENT, "exchange must be 0 (NCCL) or 1 (fused)");
+      p->exchange = (int)value;
+      return CTIS_OK;
     case CTIS_OPT_FUSED_RATIO:
       if (p->fused_ratio != (value != 0)) {
         for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);

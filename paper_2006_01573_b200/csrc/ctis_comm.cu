@@ -12,8 +12,10 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "ctis_comm.h"
+#include "ctis_nvls.h"
 
 namespace ctis {
 namespace {
@@ -31,6 +33,13 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   const char* (*errorString)(ncclResult_t) = nullptr;
   ncclResult_t (*getVersion)(int*) = nullptr;
+  // symmetric memory + device API (NCCL >= 2.28), for the fused exchange kernel (f-1)
+  ncclResult_t (*memAlloc)(void**, size_t) = nullptr;
+  ncclResult_t (*memFree)(void*) = nullptr;
+  ncclResult_t (*windowRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
+  ncclResult_t (*windowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
+  ncclResult_t (*devCommCreate)(ncclComm_t, const void*, void*) = nullptr;
+  ncclResult_t (*devCommDestroy)(ncclComm_t, const void*) = nullptr;
 };
 
 const NcclApi& api() {
@@ -53,6 +62,12 @@ const NcclApi& api() {
     a.allReduce = reinterpret_cast<decltype(a.allReduce)>(sym("ncclAllReduce"));
     a.errorString = reinterpret_cast<decltype(a.errorString)>(sym("ncclGetErrorString"));
     a.getVersion = reinterpret_cast<decltype(a.getVersion)>(sym("ncclGetVersion"));
+    a.memAlloc = reinterpret_cast<decltype(a.memAlloc)>(sym("ncclMemAlloc"));
+    a.memFree = reinterpret_cast<decltype(a.memFree)>(sym("ncclMemFree"));
+    a.windowRegister = reinterpret_cast<decltype(a.windowRegister)>(sym("ncclCommWindowRegister"));
+    a.windowDeregister = reinterpret_cast<decltype(a.windowDeregister)>(sym("ncclCommWindowDeregister"));
+    a.devCommCreate = reinterpret_cast<decltype(a.devCommCreate)>(sym("ncclDevCommCreate"));
+    a.devCommDestroy = reinterpret_cast<decltype(a.devCommDestroy)>(sym("ncclDevCommDestroy"));
     a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.reduceScatter && a.allGather && a.allReduce &&
            a.errorString;
     if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
@@ -126,6 +141,68 @@ bool nccl_all_reduce_f32(const float* send, float* recv, size_t count, void* com
   ncclResult_t r = api().allReduce(send, recv, count, ncclFloat32, ncclSum, static_cast<ncclComm_t>(comm), s);
   if (r != ncclSuccess) *err = nccl_msg("ncclAllReduce", r);
   return r == ncclSuccess;
+}
+
+bool nvls_setup(void* nccl_comm, size_t bytes, int device, NvlsComm* out, std::string* err) {
+  const NcclApi& a = api();
+  if (!a.ok || !a.memAlloc || !a.windowRegister || !a.devCommCreate) {
+    *err = "NCCL symmetric memory / device API unavailable (needs NCCL >= 2.28)";
+    return false;
+  }
+  ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
+  NvlsComm c;
+  c.bytes = (bytes + 4095) & ~size_t(4095);
+  ncclResult_t r = a.memAlloc(&c.buf, c.bytes);
+  if (r != ncclSuccess) {
+    *err = nccl_msg("ncclMemAlloc", r);
+    return false;
+  }
+  ncclWindow_t win = nullptr;
+  r = a.windowRegister(comm, c.buf, c.bytes, &win, NCCL_WIN_COLL_SYMMETRIC);
+  if (r != ncclSuccess) {
+    a.memFree(c.buf);
+    *err = nccl_msg("ncclCommWindowRegister", r);
+    return false;
+  }
+  c.window = win;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  c.blocks = 2 * sms;
+  const bool mc = !std::getenv("CTIS_NVLS_NO_MULTIMEM");  // try NVLS first; NCCL refuses it where unsupported
+  std::vector<uint64_t> reqs((devcomm_requirements_bytes() + 7) / 8, 0);
+  c.devcomm = ::operator new(devcomm_bytes());
+  memset(c.devcomm, 0, devcomm_bytes());
+  r = ncclInvalidUsage;
+  if (mc) {
+    devcomm_requirements(reqs.data(), c.blocks, true);
+    r = a.devCommCreate(comm, reqs.data(), c.devcomm);
+  }
+  if (r != ncclSuccess) {  // no multimem: NVLink peer loads / stores
+    devcomm_requirements(reqs.data(), c.blocks, false);
+    r = a.devCommCreate(comm, reqs.data(), c.devcomm);
+  }
+  if (r != ncclSuccess) {
+    a.windowDeregister(comm, win);
+    a.memFree(c.buf);
+    ::operator delete(c.devcomm);
+    *err = nccl_msg("ncclDevCommCreate", r);
+    return false;
+  }
+  c.multimem = devcomm_has_multimem(c.devcomm) && devcomm_lsa_size(c.devcomm) > 1 ? 1 : 0;
+  if (std::getenv("CTIS_NVLS_NO_MULTIMEM")) c.multimem = 0;
+  *out = c;
+  return true;
+}
+
+void nvls_teardown(void* nccl_comm, NvlsComm* c) {
+  const NcclApi& a = api();
+  if (!c || !c->buf || !a.ok) return;
+  ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
+  if (a.devCommDestroy && c->devcomm) a.devCommDestroy(comm, c->devcomm);
+  if (a.windowDeregister && c->window) a.windowDeregister(comm, static_cast<ncclWindow_t>(c->window));
+  if (a.memFree) a.memFree(c->buf);
+  ::operator delete(c->devcomm);
+  *c = NvlsComm();
 }
 
 }  // namespace ctis

@@ -353,7 +353,44 @@ def test_band_sharded_nccl_single_rank_vs_oracle(ctis, oracle_lib, dev, case):
     comm.close()
 
 
-def _nccl_worker(rank, world, port, q):
+@pytest.mark.parametrize("case", ["C2", "wrap"])
+def test_fused_nvlink_exchange_single_rank_vs_oracle(ctis, oracle_lib, dev, case):
+    """CTIS_OPT_EXCHANGE = 1: the exchange buffer is an NCCL symmetric-memory window
+    and ONE kernel reduces each rank's pixel slice over all ranks, forms r and stores it to every rank.
+    On this one-GPU box the team has one rank (peer-pointer path; NVLS multimem needs >= 2 GPUs on
+    NVSwitch): the slicing, the LSA barriers and the ratio are exercised, against the oracle."""
+    if case == "wrap":
+        geom = syn.Geometry(33, 17, 6, 70, 45)
+        taps = syn.random_taps(geom, (2, 9), seed=77, region="any")
+        K, ftrue = 25, syn.scene_random(geom, seed=3, lo=0.1)
+    else:
+        cfg = syn.config(case)
+        geom, taps, K, ftrue = cfg.geom, syn.paper_taps(cfg), cfg.K, syn.scene_blobs(cfg.geom)
+    g_np = oracle_lib.forward(geom, taps, ftrue).astype(np.float32)
+    try:
+        comm = ctis.Comm(1, 0, ctis.comm_unique_id(), 0)
+    except ctis.CtisError as e:
+        pytest.skip(f"NCCL unavailable: {e}")
+    shard = ctis.Plan.from_geometry(geom, taps, band_range=(0, geom.w))
+    shard.set_option(ctis.OPT_EXCHANGE, 1)
+    f = torch.ones(geom.m, device=dev)
+    try:
+        shard.mlem_band_sharded(comm, cuda(g_np, dev), f, K)
+    except ctis.CtisError as e:
+        if e.status == ctis.ERR_UNSUPPORTED:
+            pytest.skip(f"NCCL symmetric memory unavailable: {e}")
+        raise
+    torch.cuda.synchronize()
+    want = oracle_lib.mlem(geom, taps, g_np, np.ones(geom.m), K)
+    check(f.cpu().numpy(), want, MLEM_TOL, f"{case} fused NVLink exchange (1 rank) K={K}")
+    f2 = torch.ones(geom.m, device=dev)
+    shard.set_option(ctis.OPT_EXCHANGE, 0)
+    shard.mlem_band_sharded(comm, cuda(g_np, dev), f2, K)
+    assert rel(f2.cpu().numpy(), f.cpu().numpy()) <= 1e-5
+    comm.close()
+
+
+def _nccl_worker(rank, world, port, q, exchange=0):
     import os as _os
     import torch.distributed as tdist
     _os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -367,6 +404,7 @@ def _nccl_worker(rank, world, port, q):
     g_np = oracle.forward(geom, taps, syn.scene_blobs(geom)).astype(np.float32)
     b0, b1 = dm.band_partition(geom.w, world)[rank]
     shard = m.Plan.from_geometry(geom, taps, device=rank, band_range=(b0, b1))
+    shard.set_option(m.OPT_EXCHANGE, exchange)
     comm = dm.make_comm(rank)
     f = torch.ones(shard.m, device=f"cuda:{rank}")
     shard.mlem_band_sharded(comm, torch.from_numpy(g_np).cuda(rank), f, cfg.K)
@@ -377,8 +415,10 @@ def _nccl_worker(rank, world, port, q):
     tdist.destroy_process_group()
 
 
-def test_band_sharded_nccl_multi_gpu_vs_oracle(ctis, oracle_lib):
-    """Two ranks on two GPUs (runs only where >= 2 GPUs are visible)."""
+@pytest.mark.parametrize("exchange", [0, 1])
+def test_band_sharded_nccl_multi_gpu_vs_oracle(ctis, oracle_lib, exchange):
+    """Two ranks on two GPUs (runs only where >= 2 GPUs are visible): NCCL collectives (0) and the fused
+    NVLink exchange kernel (1)."""
     if torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs (this gpurun box exposes one)")
     import socket
@@ -387,7 +427,7 @@ def test_band_sharded_nccl_multi_gpu_vs_oracle(ctis, oracle_lib):
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
     q = mp.get_context("spawn").SimpleQueue()
-    mp.start_processes(_nccl_worker, args=(2, port, q), nprocs=2, start_method="spawn", join=True)
+    mp.start_processes(_nccl_worker, args=(2, port, q, exchange), nprocs=2, start_method="spawn", join=True)
     cfg = syn.config("C2")
     geom, taps = cfg.geom, syn.paper_taps(cfg)
     g_np = oracle_lib.forward(geom, taps, syn.scene_blobs(geom)).astype(np.float32)
