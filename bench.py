@@ -47,9 +47,55 @@ def parse():
     ap.add_argument("--mode", default="frames", choices=["frames", "bands"])
     ap.add_argument("--iters", type=int, default=None, help="MLEM iterations per reconstruction (default: config K)")
     ap.add_argument("--frames", type=int, default=None, help="frames per rank (default: 1; C5: 256/N)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
+                    help="--mode bands: NCCL reduce-scatter/all-gather or the fused NVLink exchange kernel")
+    ap.add_argument("--extra", default="C5,C3",
+                    help="N = 1: also time these workloads (same rules) under 'extra_workloads' ('' = none)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
+
+
+def time_extra(name, dev, steps=2, warmup=1):
+    """One secondary workload measured like the headline (f0 = 1 reset and 512 MB L2 flush outside the
+    CUDA events, K iterations per reconstruction, all frames of the config in one batched call)."""
+    import torch
+
+    import paper_2006_01573_b200 as ctis
+    cfg = syn.config(name)
+    geom = cfg.geom
+    taps = syn.paper_taps(cfg)
+    plan = ctis.Plan.from_geometry(geom, taps, device=dev.index or 0)
+    plan.set_option(ctis.OPT_VALIDATE_DATA, 0)
+    F = cfg.frames
+    scenes = torch.from_numpy(np.stack([syn.frame_scene(geom, i).reshape(-1) for i in range(F)]) if F > 1
+                              else syn.scene_blobs(geom).reshape(1, -1)).to(dev)
+    g = plan.forward(scenes.view(F, geom.m) if F > 1 else scenes.view(-1))
+    del scenes
+    f = torch.ones((F, geom.m) if F > 1 else (geom.m,), dtype=torch.float32, device=dev)
+    ws = plan.workspace(F)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        f.fill_(1.0)
+        plan.mlem(g, f, cfg.K, ws=ws)
+    launches = plan.last_launch_count()
+    ms = []
+    for _ in range(steps):
+        f.fill_(1.0)
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        plan.mlem(g, f, cfg.K, ws=ws)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    t = sum(ms) / len(ms)
+    return {"value": F * cfg.K / (t / 1e3), "unit": "iterations/s", "recon_per_s": F / (t / 1e3),
+            "ms_per_step": t, "steps": steps, "warmup": warmup, "frames": F, "iterations_per_step": cfg.K,
+            "us_per_frame_iteration": t * 1e3 / (F * cfg.K), "gpu_launches_per_step": launches,
+            "config": {"workload": name, "a": geom.a, "alpha": geom.alpha, "w": geom.w, "gamma": geom.gamma,
+                       "xi": geom.xi, "taps_per_band": int(taps.ptr[1])}}
 
 
 def load_peaks():
@@ -285,6 +331,7 @@ def main():
     if mode == "bands":
         comm = dmod.make_comm(local)                      # NCCL communicator owned by libctis
         ws_sh = plan.band_sharded_workspace(comm)
+        plan.set_option(ctis.OPT_EXCHANGE, 1 if args.exchange == "fused" else 0)
 
     def one_step(fb):
         if mode == "bands":
@@ -394,7 +441,8 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "mode": mode, "a": geom.a, "alpha": geom.alpha, "w": geom.w,
                        "gamma": geom.gamma, "xi": geom.xi, "taps_per_band": int(taps.ptr[1]),
-                       "iterations_per_step": K, "frames_per_rank": frames, "parallelism":
+                       "iterations_per_step": K, "frames_per_rank": frames,
+                       "exchange": args.exchange if mode == "bands" else None, "parallelism":
                        f"{'frames' if mode == 'frames' else 'bands'}{world}",
                        "l2": "flushed between timed steps (512 MB write, outside the step events)"},
             "recon_per_s": recon_total / (total_ms / 1e3),
@@ -434,6 +482,16 @@ def main():
     if line is not None and world == 1 and not args.no_cpu_baseline:
         gnp = (g if frames == 1 else g[0]).double().cpu().numpy()
         line["cpu_baseline"] = cpu_baseline(cfg, taps, gnp, K, args.workload)
+    if line is not None and world == 1 and mode == "frames" and args.extra:
+        import torch as _t
+        extra = {}
+        for name in [x for x in args.extra.split(",") if x and x != args.workload]:
+            try:
+                extra[name] = time_extra(name, dev)
+            except Exception as exc:  # report, never hide the headline line
+                extra[name] = {"error": str(exc)[:200]}
+            _t.cuda.empty_cache()
+        line["extra_workloads"] = extra
     if line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -876,9 +876,10 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
   if (!throughput && !shard && p->tma_f && !std::getenv("CTIS_NO_TPUT")) {
     ctis_plan tp = nullptr;
     ctis_status ts = build_plan(a, alpha, w, gamma, xi, tap_ptr, tap_offset, tap_weight, b0, b1, shard, device, &tp, true);
-    if (ts) {
-      delete p;
-      return ts;
+    if (ts) {  // e.g. a band too dense for NB = 12 chunks in one page: keep the single-frame layout only
+      *out = p;
+      g_last_error.clear();
+      return CTIS_OK;
     }
     size_t fc = 0, tfc = 0;
     for (const Page& pg : p->fwd) fc += pg.nchunks;

@@ -78,6 +78,8 @@ def make_comm(device: int, group=None):
     import torch.distributed as dist
 
     import paper_2006_01573_b200 as ctis
+    if not dist.is_initialized():  # a single process: a one-rank communicator, no side channel needed
+        return ctis.Comm(1, 0, ctis.comm_unique_id(), device)
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     obj = [ctis.comm_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
