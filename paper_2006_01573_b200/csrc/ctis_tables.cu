@@ -801,10 +801,7 @@ __device__ __forceinline__ void nan_fill_smem(int nf) {
 #ifndef CTIS_BACK_REFILL
 #define CTIS_BACK_REFILL 0
 #endif
-#ifndef CTIS_BACK_PREFETCH_F
-#define CTIS_BACK_PREFETCH_F 0
-#endif
-template <int NB, int POS, bool REFILL = CTIS_BACK_REFILL, bool PREF = CTIS_BACK_PREFETCH_F>
+template <int NB, int POS, bool REFILL = CTIS_BACK_REFILL>
 __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtensorMap* tm) {
   constexpr int TC = 8 * POS;
   extern __shared__ __align__(128) float smem[];
@@ -925,20 +922,6 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
     for (int k4 = 0; k4 < POS; ++k4)
 #pragma unroll
       for (int q = 0; q < BP; ++q) acc[k4][q] = make_float2(0.f, 0.f);
-    if (PREF && A.mode && q_r0 + lane < A.a) {
-      // pull this item's f tile (read again by the epilogue, ~one item later) into L1 now, so the
-      // epilogue's loads hit L1 instead of waiting on L2 (ncu: long-scoreboard stalls in the epilogue)
-      const float* fz = A.dst + (long long)z * A.dst_frame;
-#pragma unroll 1
-      for (int b = 0; b < nb; ++b)
-#pragma unroll
-        for (int k4 = 0; k4 < POS; ++k4) {
-          const int qc = q_c0 + warp + NWARPS * k4;
-          if (qc < A.alpha)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(fz + (long long)(lam0 + b) * A.ell + q_r0 + lane +
-                                                          (long long)A.a * qc));
-        }
-    }
     auto compute = [&](unsigned ba, int c) {
       const uint4* ent = tab4(TP) + c * BP;
 #pragma unroll
