@@ -8,7 +8,7 @@ EXTRA    ?=
 LIBOUT   ?= $(PKG)/libctis.so
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden \
             --expt-relaxed-constexpr -Iinclude $(EXTRA)
-HDRS     := include/ctis.h $(PKG)/csrc/ctis_internal.h $(PKG)/csrc/ctis_kernels.h $(PKG)/csrc/ctis_fft.h \
+HDRS     := include/ctis.h $(PKG)/csrc/ctis_internal.h $(PKG)/csrc/ctis_strip_dispatch.inc $(PKG)/csrc/ctis_kernels.h $(PKG)/csrc/ctis_fft.h \
             $(PKG)/csrc/ctis_comm.h $(PKG)/csrc/ctis_nvls.h
 # nccl.h for the latency mode's types (the library itself is dlopen'ed at run time)
 NCCL_INC ?= $(shell python -c "import os, nvidia.nccl as m; print(os.path.join(list(m.__path__)[0], 'include'))" 2>/dev/null || echo /usr/include)

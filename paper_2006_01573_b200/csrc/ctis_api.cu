@@ -94,6 +94,8 @@ struct Page {
   int max_modes = 0;
   int total_items = 0;  // tiles summed over the page's chunks (persistent kernels)
   int back_tc = 32;     // back pages: tile columns (kernel family)
+  bool strip = false;   // forward pages: strip kernel (ctis_fwd_strip_t)
+  int strip_warps = 0;  // strip pages: consumer warps (max strip groups over the page's chunks)
   std::vector<uint32_t> words;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
@@ -114,6 +116,7 @@ struct ctis_plan_s {
   int back_tc = kBackTC;  // back tile columns: 32, or 16 for small TMA plans (ctis_back2_*)
   int fbox_r = 0, fbox_c = 0, bbox_r = 0, bbox_c = 0;
   int fwd_g = 1, fwd_m = 8;
+  bool fwd_strip = false;  // forward pages use the strip kernel (ctis_tables.cu forward_strip)
   int sms = 148;
   bool pair = false;  // FFMA2 on tap pairs (16-byte entries) or plain FFMA (8-byte entries)
   bool nowrap = false;  // no tap carries across FPA columns or wraps past n (2-D translations only)
@@ -424,6 +427,231 @@ void pack_pages(std::vector<Page>& pages, bool forward, const std::vector<std::v
   flush();
 }
 
+// ------------------------------------------------------------------------------------------------
+// Strip forward layout (ctis_internal.h "Strip forward").  Modes of a chunk whose column shift
+// dc (relative to the mode reference) is identical in every band form a column group; a column
+// group is cut into strip groups of <= kStripMG modes, sorted along their drift, such that in
+// every band the row offsets of the group's taps span at most kStripNO - 1 rows of one strip.
+struct StripGroup {
+  std::vector<const Mode*> ms;
+};
+
+// per band, per mode: row / column of the window that position 0 of the u strip reads
+struct StripPass {
+  int b0 = 0, nb = 0;
+  std::vector<StripGroup> groups;
+};
+
+std::vector<StripGroup> strip_groups(int nb, const std::vector<Mode>& modes) {
+  const int bref = (nb - 1) / 2;
+  // column signature: dc relative to the reference per band (INT_MIN where the mode has no tap)
+  std::map<std::vector<int>, std::vector<const Mode*>> cols;
+  for (const Mode& md : modes) {
+    std::vector<int> sig(nb, INT_MIN);
+    for (const ModeTap& t : md.taps) sig[t.b] = t.dc - md.ref_dc;
+    cols[sig].push_back(&md);
+  }
+  std::vector<StripGroup> out;
+  for (auto& kv : cols) {
+    std::vector<const Mode*> ms = kv.second;
+    // order along the drift: sum_b (b - bref) * dr_rel (modes of one diffraction-order column
+    // line up by order index p)
+    auto key = [&](const Mode* md) {
+      long long k = 0;
+      for (const ModeTap& t : md->taps) k += (long long)(t.b - bref) * (t.dr - md->ref_dr);
+      return k;
+    };
+    std::stable_sort(ms.begin(), ms.end(), [&](const Mode* x, const Mode* y) { return key(x) < key(y); });
+    // greedy cut: extend the current group while every band's row-offset range (incl. 4-row
+    // alignment of the strip start) stays within kStripNO - 1
+    std::vector<int> lo(nb, INT_MAX), hi(nb, INT_MIN);
+    StripGroup cur;
+    auto fits = [&](const Mode* md) {
+      if ((int)cur.ms.size() >= kStripMG) return false;
+      for (const ModeTap& t : md->taps) {
+        const int d = t.dr - md->ref_dr;
+        const int l = std::min(lo[t.b], d), h = std::max(hi[t.b], d);
+        if (h - l + 3 > kStripNO - 1) return false;
+      }
+      return true;
+    };
+    for (const Mode* md : ms) {
+      if (!fits(md)) {
+        out.push_back(cur);
+        cur = StripGroup();
+        std::fill(lo.begin(), lo.end(), INT_MAX);
+        std::fill(hi.begin(), hi.end(), INT_MIN);
+      }
+      cur.ms.push_back(md);
+      for (const ModeTap& t : md->taps) {
+        const int d = t.dr - md->ref_dr;
+        lo[t.b] = std::min(lo[t.b], d);
+        hi[t.b] = std::max(hi[t.b], d);
+      }
+    }
+    if (!cur.ms.empty()) out.push_back(cur);
+  }
+  return out;
+}
+
+// Strip chunk descriptor for one pass (bands [b0, b0+nb), its strip groups); box_r / box_c are the
+// plan's TMA box.  need_r / need_c report the box this pass needs (first call with box_r = 0).
+bool strip_desc(const ctis_plan_s& P, const StripPass& ps, int box_r, std::vector<uint32_t>& out, int& tiles,
+                int& need_r, int& need_c) {
+  const int nb = ps.nb, nhg = (int)ps.groups.size();
+  std::vector<const Mode*> all_ms;
+  for (const StripGroup& g : ps.groups) all_ms.insert(all_ms.end(), g.ms.begin(), g.ms.end());
+  const std::vector<Span> sp = band_spans(nb, all_ms);
+  Span all;
+  for (const Span& x : sp)
+    if (!x.empty()) {
+      all.add(x.rmin, x.cmin);
+      all.add(x.rmax, x.cmax);
+    }
+  out.clear();
+  tiles = 0;
+  need_r = need_c = 0;
+  if (all.empty()) return true;
+  // u-tile row origins u_r0 + 32k are multiples of 4 and so are the mode reference rows
+  // (build_strip_forward): every flush box starts on a 16-byte FPA row boundary (TMA reduce)
+  all.rmin = (int)std::floor(all.rmin / 4.0) * 4;
+  const int tiles_r = (P.a + all.rmax - all.rmin + kFwdTR - 1) / kFwdTR;
+  const int tiles_c = (P.alpha + all.cmax - all.cmin + kFwdTC - 1) / kFwdTC;
+  const int BI = kDescHeader + kStripMG * nhg, TP = BI + 4 * nb;
+  out.assign(TP + 8 * nb * nhg, 0u);
+  out[0] = (uint32_t)ps.b0;
+  out[1] = (uint32_t)nb;
+  out[2] = (uint32_t)nhg;
+  out[3] = (uint32_t)all.rmin;
+  out[4] = (uint32_t)all.cmin;
+  out[5] = (uint32_t)tiles_r;
+  out[6] = (uint32_t)tiles_c;
+  for (int g = 0; g < nhg; ++g)
+    for (int k = 0; k < kStripMG; ++k) {
+      const Mode* md = k < (int)ps.groups[g].ms.size() ? ps.groups[g].ms[k] : nullptr;
+      out[kDescHeader + kStripMG * g + k] = md ? (uint32_t)(md->ref_dr + P.gamma * md->ref_dc) : 0xffffffffu;
+    }
+  for (int b = 0; b < nb; ++b) {
+    // TMA box row origin all.rmin + 32k + row0_rel must be a multiple of 4 (see forward_desc)
+    const int rmax = sp[b].empty() ? 0 : sp[b].rmax, cmax = sp[b].empty() ? 0 : sp[b].cmax;
+    const int lead = (int)((((long long)all.rmin - rmax) % 4 + 4) % 4);
+    out[BI + 4 * b + 0] = (uint32_t)(-rmax - lead);
+    out[BI + 4 * b + 1] = (uint32_t)(-cmax);
+    if (!sp[b].empty()) need_c = std::max(need_c, kFwdTC + sp[b].cmax - sp[b].cmin);
+    for (int g = 0; g < nhg; ++g) {
+      const int e = TP + 8 * (b * nhg + g);
+      out[e + 1] = 0x01010101u * (uint32_t)kStripNO;  // every slot skips
+      int rlo = INT_MAX, rhi = INT_MIN, ccol = INT_MIN;
+      int R[kStripMG];
+      float W[kStripMG];
+      for (int k = 0; k < kStripMG; ++k) R[k] = INT_MIN, W[k] = 0.f;
+      for (int k = 0; k < (int)ps.groups[g].ms.size(); ++k) {
+        const Mode* md = ps.groups[g].ms[k];
+        for (const ModeTap& t : md->taps) {
+          if (t.b != b) continue;
+          const int c = cmax - (t.dc - md->ref_dc);
+          if (ccol != INT_MIN && c != ccol) return false;  // column groups share dc by construction
+          ccol = c;
+          R[k] = rmax + lead - (t.dr - md->ref_dr);
+          W[k] = t.w;
+          rlo = std::min(rlo, R[k]);
+          rhi = std::max(rhi, R[k]);
+        }
+      }
+      if (ccol == INT_MIN) continue;  // no tap of this group in band b: nq = 0, every slot skipped
+      const int lo4 = rlo & ~3;
+      const int nq = (rhi - lo4 + kStripP + 3) / 4;
+      if (nq > kStripNQ) return false;
+      need_r = std::max(need_r, kStripP + lo4 + 4 * kStripNQ);  // every band reads the whole strip
+      if (box_r) {
+        out[e + 0] = (uint32_t)(4LL * (lo4 + (long long)box_r * ccol));
+        uint32_t opack = 0;
+        for (int k = 0; k < kStripMG; ++k) {
+          const uint32_t o = R[k] == INT_MIN ? (uint32_t)kStripNO : (uint32_t)(R[k] - lo4);
+          if (o > (uint32_t)kStripNO || (o == (uint32_t)kStripNO && R[k] != INT_MIN)) return false;
+          opack |= o << (8 * k);
+          out[e + 2 + k] = fbits(W[k]);
+        }
+        out[e + 1] = opack;
+      }
+    }
+  }
+  tiles = tiles_r * tiles_c;
+  return true;
+}
+
+// Strip layout of the whole forward (false: the plan keeps the classic forward kernels).
+bool build_strip_forward(ctis_plan_s& P, const std::vector<std::pair<int, int>>& chunks,
+                         const std::vector<std::vector<Mode>>& chunk_modes) {
+  const char* env = std::getenv("CTIS_FWD_STRIP");
+  const int want = env ? std::atoi(env) : -1;  // 0 never, 1 whenever possible, -1 when it pays
+  if (want == 0 || !P.tma_f) return false;
+  // Mode references with rows rounded down to a multiple of 4 (o = o_ref + dr + gamma*dc holds for any
+  // reference; the shifts grow by <= 3 rows): flush boxes then start on 16-byte FPA row boundaries.
+  std::vector<std::vector<Mode>> smodes = chunk_modes;  // outlives every StripGroup pointer below
+  for (auto& ms : smodes)
+    for (Mode& md : ms) md.ref_dr &= ~3;
+  std::vector<StripPass> passes;
+  size_t nmodes = 0, ngroups = 0;
+  for (size_t k = 0; k < chunks.size(); ++k) {
+    std::vector<StripGroup> gs = strip_groups(chunks[k].second, smodes[k]);
+    nmodes += smodes[k].size();
+    ngroups += gs.size();
+    const int np = (int)((gs.size() + kStripWarpsMax - 1) / kStripWarpsMax);
+    for (int i = 0; i < np; ++i) {
+      StripPass ps;
+      ps.b0 = chunks[k].first;
+      ps.nb = chunks[k].second;
+      // balanced passes: groups i, i + np, ... (neighbouring columns in different passes)
+      for (size_t g = (size_t)i; g < gs.size(); g += (size_t)np) ps.groups.push_back(gs[g]);
+      passes.push_back(std::move(ps));
+    }
+  }
+  if (ngroups == 0) return false;
+  if (want < 0) {
+    // measured on B200 (tools/gpu_strip.sh): the strip kernel wins where every chunk fits one pass of
+    // <= kStripWarpsMax groups and chunks are long (C4: 62 vs 82 us); with several passes per chunk
+    // (C3's streak taps: 17 groups) or short chunks (C2: 1-band chunks) the classic kernel is faster
+    if ((double)nmodes < 2.0 * (double)ngroups) return false;  // too little strip reuse
+    if (passes.size() != chunks.size()) return false;
+    for (auto [b0, nb] : chunks)
+      if (nb < 12) return false;
+  }
+  int box_r = 0, box_c = 1;
+  for (const StripPass& ps : passes) {
+    std::vector<uint32_t> d;
+    int t = 0, nr = 0, nc = 0;
+    if (!strip_desc(P, ps, 0, d, t, nr, nc)) return false;
+    box_r = std::max(box_r, nr);
+    box_c = std::max(box_c, nc);
+  }
+  box_r = std::max(box_r, 8);
+  while (box_r % 8 != 4) ++box_r;  // pitch / 4 odd: conflict-free float4 strip loads across columns
+  if (box_r > 256 || box_c > 256 || (long long)box_r * box_c > kTmaWinFloats) return false;
+  std::vector<std::vector<uint32_t>> descs;
+  std::vector<int> tiles, warps;
+  for (const StripPass& ps : passes) {
+    std::vector<uint32_t> d;
+    int t = 0, nr = 0, nc = 0;
+    if (!strip_desc(P, ps, box_r, d, t, nr, nc)) return false;
+    if (d.empty()) continue;
+    if (d.size() + kPageHeader > (size_t)kPageWords) return false;
+    descs.push_back(std::move(d));
+    tiles.push_back(t);
+    warps.push_back((int)ps.groups.size());
+  }
+  P.fwd.clear();
+  pack_pages(P.fwd, true, descs, tiles, warps);
+  for (Page& pg : P.fwd) {
+    pg.strip = true;
+    pg.strip_warps = pg.max_modes;
+  }
+  P.fbox_r = box_r;
+  P.fbox_c = box_c;
+  P.fwd_strip = true;
+  return true;
+}
+
 // Byte offset and size of the ".nv.constant3" section (the c_tab bank) in the embedded cubin.
 bool constant_bank_section(const unsigned char* img, size_t len, size_t& off, size_t& size) {
   if (len < 64 || std::memcmp(img, "\x7f" "ELF", 4) != 0 || img[4] != 2) return false;  // ELF64 only
@@ -478,7 +706,9 @@ ctis_status load_page(Page& pg, bool vec) {
   CTIS_CUDA(cudaLibraryLoadData(&pg.lib, img.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
             "cudaLibraryLoadData (tap page)");
   std::string name;
-  if (pg.forward) {
+  if (pg.forward && pg.strip) {
+    name = "ctis_fwd_strip_t";
+  } else if (pg.forward) {
     name = "ctis_fwd_g" + std::to_string(pg.max_modes / 1000) + "_m" + std::to_string(pg.max_modes % 1000) +
            (vec ? "_t" : "_s");
   } else {
@@ -643,6 +873,7 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
       modes.push_back(1000 * P.fwd_g + P.fwd_m);  // forward pages: "max_modes" encodes the template
     }
     pack_pages(P.fwd, true, descs, tiles, modes);
+    build_strip_forward(P, chunks, chunk_modes);  // replaces the pages when the strip layout applies
   }
   // ---- back: NB (kernel template) chosen so that tiles x chunks fills the SMs; a chunk whose
   //      descriptor would not fit one 64 KB page is split further
@@ -989,6 +1220,20 @@ cudaError_t make_tensor_map(CUtensorMap* tm, bool forward, const ctis_plan_s& P,
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// g_hat as {gamma, xi, frames} with 32 x 16 boxes and the 128-byte swizzle: the strip forward's
+// accumulator tiles are added into it with cp.reduce.async.bulk.tensor (out-of-range elements dropped).
+cudaError_t make_ghat_map(CUtensorMap* tm, const ctis_plan_s& P, float* base, int frames) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t dims[3] = {(cuuint64_t)P.gamma, (cuuint64_t)P.xi, (cuuint64_t)frames};
+  const cuuint64_t strides[2] = {4ull * P.gamma, 4ull * P.n};
+  const cuuint32_t box[3] = {(cuuint32_t)kFwdTR, (cuuint32_t)kFwdTC, 1u};
+  const cuuint32_t es[3] = {1u, 1u, 1u};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 // Launch with programmatic stream serialization (PDL): the kernel may start while its predecessor
 // drains; it waits for the predecessor's results with griddepcontrol.wait (ctis_tables.cu pdl_enter).
 cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s,
@@ -1042,11 +1287,18 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
             slot, box_r, box_c, (unsigned)(4 * box_r * ((debug_flags() & 32) ? std::max(1, box_c / 2) : box_c)),
             debug_flags(), frames, P.nowrap ? 1 : 0,
             0, nullptr, 0, P.d_gbar, nullptr, 0};
-  alignas(64) CUtensorMap tm;
+  alignas(64) CUtensorMap tm, tg;
   std::memset(&tm, 0, sizeof(tm));
+  std::memset(&tg, 0, sizeof(tg));
   if (tma) {
     cudaError_t e = make_tensor_map(&tm, fwd, P, src, frames);
     if (e != cudaSuccess) return e;
+  }
+  A.tma_flush = 0;
+  if (fwd && P.fwd_strip && P.nowrap && P.gamma % 4 == 0) {  // strip forward: g_hat as a TMA reduce target
+    cudaError_t e = make_ghat_map(&tg, P, dst, frames);
+    if (e != cudaSuccess) return e;
+    A.tma_flush = 1;
   }
   const int threads = fwd ? (P.fwd_g == 2 ? kFwd2Threads : kFwdThreads) : (tma ? kBack4Threads : kBackThreads);
   const int stages = fwd ? kFwdStages : kBackStages;
@@ -1080,8 +1332,17 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
         A.zero_count = fuse->zero_count;
       }
     }
-    void* args[] = {&A, &tm};
-    cudaError_t e = launch_pdl((const void*)pg.kern, grid, dim3(threads), args, smem, s, coop);
+    int nthreads = threads;
+    size_t nsmem = smem;
+    if (pg.strip) {  // warp-specialised strip forward: one CTA per SM, consumer warps + a producer warp
+      nthreads = 32 * (pg.strip_warps + 1);
+      // [ring][staging, 1024-byte aligned][mbarriers]; + 1 KB alignment slack of the dynamic base
+      nsmem = ((size_t)128 + kStripStages * slot * sizeof(float) + 1023) / 1024 * 1024 + 1024 +
+              (size_t)pg.strip_warps * kStripStage * sizeof(float);
+      grid = dim3((unsigned)std::min<long long>(items, (long long)P.sms), 1, 1);
+    }
+    void* args[] = {&A, &tm, &tg};
+    cudaError_t e = launch_pdl((const void*)pg.kern, grid, dim3(nthreads), args, nsmem, s, coop);
     if (e != cudaSuccess) return e;
     if (count) ++*count;
   }
@@ -1518,8 +1779,13 @@ ctis_status ctis_plan_info(ctis_plan p, int64_t out[10]) {
     fitems += pg.total_items;
   }
   for (const Page& pg : p->back) bch += pg.nchunks;
+  int64_t fwd_kind = p->fwd_m;  // classic forward: modes per group; strip forward: -(consumer warps)
+  if (p->fwd_strip) {
+    fwd_kind = 0;
+    for (const Page& pg : p->fwd) fwd_kind = std::min<int64_t>(fwd_kind, -pg.strip_warps);
+  }
   const int64_t v[10] = {(int64_t)p->fwd.size(), (int64_t)p->back.size(), fch, bch, p->tma_f ? 1 : 0,
-                         p->tma_b ? 1 : 0, p->back_nb, p->back_tc, p->fwd_m, fitems};
+                         p->tma_b ? 1 : 0, p->back_nb, p->back_tc, fwd_kind, fitems};
   std::memcpy(out, v, sizeof(v));
   return CTIS_OK;
 }

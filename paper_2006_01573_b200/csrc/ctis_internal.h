@@ -63,6 +63,29 @@ constexpr int kFwdWinFloats = 2560;     // element-loader slot: 10 KB per stage 
 constexpr int kTmaWinFloats = 8192;     // TMA box cap (32 KB)
 constexpr int kBackWinFloats = 3584;    // 14 KB per stage (>= 60 x 56)
 
+// Strip forward (forward_strip, TMA plans whose modes share column drifts — every diffraction order
+// (p, q) of a band chunk drifts by (p, q) * d'(lambda), so the orders of one q column move together):
+// a warp owns a 32 x 16 u-tile as 32 strips of kStripP consecutive rows (lane = rs + 2*column) and a
+// "strip group" of <= kStripMG modes with identical column shifts.  Per band it loads ONE register
+// strip of <= 4*kStripNQ window rows and every mode of the group reads its 16 rows from it at its own
+// row offset o in [0, kStripNO): one shared-memory word feeds ~2.4 FMAs instead of one.
+//
+// Strip chunk descriptor (forward pages with kind = strip):
+//   [D+0] lam0 [D+1] nb [D+2] nhg (strip groups = consumer warps used) [D+3] u_r0 [D+4] u_c0
+//   [D+5] tiles_r [D+6] tiles_c [D+7] 0
+//   [D+8 ..]          o_ref[g*kStripMG + k] (0xffffffff: empty slot)     (4*nhg words)
+//   [BI ..]           per band: row0_rel, col0_rel, 0, 0
+//   [TP = BI+4*nb ..] per band b and group g: 8 words at TP + 8*(b*nhg + g):
+//                     [0] strip byte offset into the window (thread base excluded), [1] row offset o_k
+//                     of slot k in byte k (kStripNO: no tap), [2..5] w_k, [6..7] 0
+constexpr int kStripP = 16;   // rows per thread strip
+constexpr int kStripMG = 4;   // modes per strip group (accumulators: kStripMG x kStripP per thread)
+constexpr int kStripNQ = 10;  // max float4 loads per strip (40 window rows)
+constexpr int kStripNO = 4 * kStripNQ - kStripP + 1;  // row offsets 0..24 (one code block per offset)
+constexpr int kStripWarpsMax = 14;  // consumer warps per CTA (+ 1 TMA producer warp): <= 136 registers
+constexpr int kStripStages = 6;
+constexpr int kStripStage = kStripMG * 512;  // flush staging floats per warp (kStripMG tiles of 16 x 32)
+
 // Per-launch parameters of the table kernels.
 struct TabArgs {
   const float* src;    // forward: f; back: r
@@ -89,6 +112,9 @@ struct TabArgs {
   // back kernel: zero zero_count floats at zero_buf (the next iteration's g_hat accumulator)
   float* zero_buf;
   long long zero_count;
+  // strip forward: flush accumulator tiles with TMA bulk reduce-add through the g_hat tensor map
+  // (nowrap plans with 16-byte FPA column strides); otherwise red.global.add with modular indices
+  int tma_flush;
 };
 
 }  // namespace ctis

@@ -29,6 +29,8 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "ctis_internal.h"
 
 using namespace ctis;
@@ -1005,6 +1007,242 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
 #endif
 }
 
+// ------------------------------------------------------------------------------------------------
+// Strip forward (ctis_internal.h, "Strip forward").  The same u-space accumulation as
+// forward_persistent2 — acc[mode](u) += w * f_lam[u - (dr, dc)], flushed to g_hat[E(u) + o_ref]
+// (Eqs. 11-13) — but a warp owns a strip group of <= kStripMG modes whose column shift dc is the same
+// in every band of the chunk, and each thread owns kStripP consecutive rows of one u column.  Per band
+// the thread loads one strip of window rows into registers (<= kStripNQ float4) and every mode of the
+// group reads its kStripP operands from that strip at its own row offset o: the offset is a run-time
+// value, so each (mode slot, o) pair is its own straight-line block (FFMA2 for even o) selected by a
+// warp-uniform switch.  Warp specialisation: the last warp's lane 0 produces the TMA windows into a
+// kStripStages ring (full / empty mbarriers), the consumer warps release a slot as soon as their strip
+// is in registers.
+#include "ctis_strip_dispatch.inc"
+
+// one lane of the (converged) warp; elect.sync also orders the warp's earlier shared loads before the
+// elected lane's release (it synchronises the warp like __syncwarp)
+__device__ __forceinline__ bool elect_one() {
+  unsigned p;
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\nselp.u32 %0, 1, 0, e;\n}\n"
+      : "=r"(p)
+      :
+      : "memory");
+  return p != 0;
+}
+
+// g_hat tile reduction by the async proxy: out[(r0 + i) + gamma*(c0 + j) (+ n*z)] += tile[j][i] for the
+// 32 x 16 box at shared address src (TMA, add).  Measured on B200 (tools/tma_red_test.cu): the box must
+// start inside the tensor on a 16-byte boundary of the inner dimension, else the instruction faults.
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* tm, unsigned src, int r0, int c0, int z) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
+      "r"(r0), "r"(c0), "r"(z), "r"(src)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int MG>
+__device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CUtensorMap* tg, int warp, int lane,
+                                                      int per_frame, int nch, int items, unsigned sbase,
+                                                      unsigned slot_bytes, unsigned full, unsigned empty,
+                                                      unsigned stage);
+
+template <int MG>
+__device__ __forceinline__ void forward_strip(const TabArgs& A, const CUtensorMap* tm, const CUtensorMap* tg) {
+  extern __shared__ __align__(1024) float smem[];
+  constexpr int S = kStripStages;
+  static_assert(MG == kStripMG, "descriptor layout assumes kStripMG slots per group");
+  const int nch = tabi(0);
+  const int per_frame = tabi(kItemBase + nch);
+  const int items = per_frame * A.frames;
+  if ((int)blockIdx.x >= items) return;
+  // warp index made visibly warp-uniform (keeps the tap entries on the uniform datapath)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const int nwc = (int)(blockDim.x >> 5) - 1;  // consumer warps; warp nwc is the TMA producer
+  const unsigned smem0 = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned slot_bytes = 4u * A.slot_floats;
+  // [full S][empty S] mbarriers | ring: S slots from byte 128 | staging: 1024-byte aligned, kStripStage
+  // floats per consumer warp.  Every address is uniform (no per-band rematerialisation from blockDim).
+  const unsigned full = smem0, empty = smem0 + 8 * S;
+  const unsigned sbase = smem0 + 128;
+  const unsigned stage0 = (sbase + S * slot_bytes + 1023u) & ~1023u;
+  static_assert(16 * S <= 128, "mbarriers fit below the ring");
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + 8 * s, 1);
+      mbar_init(empty + 8 * s, (unsigned)nwc);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == nwc) {  // ---- producer: one TMA box per (item, band), in the consumers' order
+    if (lane == 0 && !(A.dbg & 1)) {
+      unsigned slot = 0, phase = 0, w = 0;
+      for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        int z, k, tile;
+        decode_item(it, per_frame, nch, z, k, tile);
+        const uint32_t D = c_tab[1 + k];
+        const int lam0 = tabi(D + 0), nb = tabi(D + 1), nhg = tabi(D + 2), tiles_r = tabi(D + 5);
+        const int U_r = tabi(D + 3) + (tile % tiles_r) * kFwdTR, U_c = tabi(D + 4) + (tile / tiles_r) * kFwdTC;
+        const uint32_t BI = D + kDescHeader + MG * nhg;
+#pragma unroll 1
+        for (int b = 0; b < nb; ++b, ++w) {
+          if (w >= (unsigned)S) mbar_wait(empty + 8 * slot, phase ^ 1u);  // consumers released the slot
+          mbar_expect_tx(full + 8 * slot, A.box_bytes);
+          tma_4d(sbase + slot * slot_bytes, tm, U_r + tabi(BI + 4 * b), U_c + tabi(BI + 4 * b + 1), lam0 + b, z,
+                 full + 8 * slot);
+          if (++slot == (unsigned)S) {
+            slot = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else {
+    forward_strip_consume<MG>(A, tg, warp, lane, per_frame, nch, items, sbase, slot_bytes, full, empty,
+                              stage0 + 4u * kStripStage * warp);
+  }
+  if (A.ratio_mode) {  // fused ratio (CTIS_OPT_FUSED_RATIO): one CTA per SM, cooperative launch
+    grid_sync(A.gbar);
+    ratio_pass(A);
+  }
+}
+
+template <int MG>
+__device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CUtensorMap* tg, int warp, int lane,
+                                                      int per_frame, int nch, int items, unsigned sbase,
+                                                      unsigned slot_bytes, unsigned full, unsigned empty,
+                                                      unsigned stage) {
+  constexpr int S = kStripStages, NV = 4 * kStripNQ;
+  // ---- consumers: lane = rs + 2*col owns rows 16*rs .. 16*rs+15 of u column col of the 32 x 16 tile
+  const int rs = lane & 1, col = lane >> 1;
+  unsigned tb = sbase + 4u * (kStripP * rs + A.box_r * col);
+  // opaque copies: ptxas would otherwise re-derive these addresses (S2R, LDC) in every band iteration
+  asm volatile("mov.b32 %0, %0;" : "+r"(tb));
+  asm volatile("mov.b32 %0, %0;" : "+r"(full));
+  asm volatile("mov.b32 %0, %0;" : "+r"(empty));
+  // async-proxy flush: the whole plan is 2-D translations (every nonzero accumulator's pixel is inside
+  // the FPA box) — otherwise (cyclic wrap of Eq. 7) red.global.add with exact modular indices
+  const bool tma_flush = A.tma_flush && !(A.dbg & 1);
+  float v[NV];
+  unsigned slot = 0, phase = 0, tslot = tb;  // tslot: this thread's strip base in the current slot
+  unsigned notma = A.dbg & 1;  // profiling switch, pinned in a register (not re-read every band)
+  asm volatile("mov.b32 %0, %0;" : "+r"(notma));
+  bool staged = false;  // bulk reductions of this warp's staging tiles may still be reading them
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    int z, k, tile;
+    decode_item(it, per_frame, nch, z, k, tile);
+    const uint32_t D = c_tab[1 + k];
+    const int nb = tabi(D + 1), nhg = tabi(D + 2), tiles_r = tabi(D + 5);
+    const int U_r = tabi(D + 3) + (tile % tiles_r) * kFwdTR, U_c = tabi(D + 4) + (tile / tiles_r) * kFwdTC;
+    const bool act = warp < nhg;
+    const uint4* ent = tab4(D + kDescHeader + MG * nhg + 4 * nb) + 2 * warp;  // band 0, this warp's group
+    const unsigned estep = 2u * nhg;
+    float acc[MG][kStripP];
+#pragma unroll
+    for (int m = 0; m < MG; ++m)
+#pragma unroll
+      for (int i = 0; i < kStripP; ++i) acc[m][i] = 0.f;
+    // tap entries are software-pipelined one band ahead (constant-cache latency overlaps a band's FMAs)
+    uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = e0;
+    if (act) {
+      e0 = ent[0];
+      e1 = ent[1];
+    }
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+      const uint4 c0 = e0, c1 = e1;
+      if (act && b + 1 < nb) {
+        ent += estep;
+        e0 = ent[0];
+        e1 = ent[1];
+      }
+      if (!notma) mbar_wait(full + 8 * slot, phase);
+      // the whole 40-row strip (rows past the group's range are never read by its blocks)
+      if (act) strip_load(v, tslot + c0.x);
+      if (elect_one()) mbar_arrive(empty + 8 * slot);  // the strip is in registers: the slot may be refilled
+      tslot += slot_bytes;
+      if (++slot == (unsigned)S) {
+        slot = 0;
+        phase ^= 1u;
+        tslot = tb;
+      }
+      if (act) {
+        // row offset per slot (kStripNO: no tap in this band, the skip target)
+        strip_dispatch4(acc[0], acc[1], acc[2], acc[3], v, __uint_as_float(c0.z), __uint_as_float(c0.w),
+                        __uint_as_float(c1.x), __uint_as_float(c1.y), c0.y & 0xffu, (c0.y >> 8) & 0xffu,
+                        (c0.y >> 16) & 0xffu, c0.y >> 24);
+      }
+    }
+    if (!act) continue;
+    float* g = A.dst + (long long)z * A.dst_frame;
+    if (A.dbg & 2) {  // profiling: no flush (keep the accumulators live)
+      float t = 0.f;
+#pragma unroll
+      for (int m = 0; m < MG; ++m)
+#pragma unroll
+        for (int i = 0; i < kStripP; ++i) t += acc[m][i];
+      if (t == -1.f) g[0] = t;
+      continue;
+    }
+    // Flush: each mode's 32 x 16 accumulator tile -> staging (TMA 128-byte swizzle: 16-byte chunk c of u
+    // column j lives at chunk c ^ (j & 7) of the column's 128-byte line) -> g_hat[E(u) + o_ref] +=.
+    // A tile whose 2-D FPA box lies inside the FPA (no-wrap plans) is ONE bulk tensor reduce-add drained
+    // by the async proxy while the warp moves on; any other tile (FPA edge, cyclic wrap of Eq. 7) is
+    // read back lane = row and added element by element with exact modular indices (red.global.add).
+    if (staged) {  // the previous item's bulk reductions must have read the staging tiles
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+      staged = false;
+    }
+#pragma unroll
+    for (int m = 0; m < MG; ++m) {
+      const unsigned tile_s = stage + 2048u * m + 128u * col;
+#pragma unroll
+      for (int j = 0; j < kStripP / 4; ++j)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(tile_s + 16u * ((4 * rs + j) ^ (col & 7))),
+                     "f"(acc[m][4 * j]), "f"(acc[m][4 * j + 1]), "f"(acc[m][4 * j + 2]), "f"(acc[m][4 * j + 3])
+                     : "memory");
+    }
+    fence_proxy_async();
+    __syncwarp();
+    const long long n = A.n;
+#pragma unroll 1
+    for (int m = 0; m < MG; ++m) {
+      const unsigned o = c_tab[D + kDescHeader + MG * warp + m];
+      if (o == 0xffffffffu) continue;
+      const int r0 = U_r + (int)(o % (unsigned)A.gamma), c0 = U_c + (int)(o / (unsigned)A.gamma);
+      const unsigned tile_s = stage + 2048u * m;
+      if (tma_flush && r0 >= 0 && (r0 & 3) == 0 && c0 >= 0 && r0 + kFwdTR <= A.gamma && c0 + kFwdTC <= A.xi) {
+        if (lane == 0) tma_reduce_add_3d(tg, tile_s, r0, c0, z);
+        staged = true;
+        continue;
+      }
+      const long long e_lane = (long long)(U_r + lane) + (long long)A.gamma * U_c + o;
+#pragma unroll 4
+      for (int cc = 0; cc < kFwdTC; ++cc) {
+        const float val = lds(tile_s + 128u * cc + 16u * ((lane >> 2) ^ (cc & 7)) + 4u * (lane & 3));
+        long long e = e_lane + (long long)A.gamma * cc;
+        if (!A.nowrap || (A.dbg & 1)) {  // no-wrap plans: every nonzero accumulator's index is in [0, n)
+          e %= n;
+          if (e < 0) e += n;
+        }
+        red_nz(g + e, val);
+      }
+    }
+    if (staged && lane == 0) bulk_commit();
+    __syncwarp();  // the element path's staging reads are done before the next item's writes
+  }
+  if (lane == 0) bulk_wait0();  // every bulk reduction of this warp has completed (and read its staging)
+  __syncwarp();
+}
+
 }  // namespace
 
 // Element-loader forward (plans whose geometry rules out TMA boxes: a % 4 != 0)
@@ -1101,3 +1339,12 @@ CTIS_BACK(4)
 CTIS_BACK(8)
 CTIS_BACK(12)
 CTIS_BACK(16)
+
+// Strip forward (TMA plans with column-sharing modes): kStripWarpsMax consumer warps + 1 producer
+extern "C" __global__ void __launch_bounds__(32 * (kStripWarpsMax + 1), 1)
+    ctis_fwd_strip_t(const TabArgs A, const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tg) {
+  if (A.frames == 0) return;
+  pdl_enter();
+  if (A.dbg & 8) nan_fill_smem(kStripStages * A.slot_floats);
+  forward_strip<kStripMG>(A, &tm, &tg);
+}
