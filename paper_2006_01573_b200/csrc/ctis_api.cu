@@ -562,7 +562,9 @@ bool strip_desc(const ctis_plan_s& P, const StripPass& ps, int box_r, std::vecto
       const int lo4 = rlo & ~3;
       const int nq = (rhi - lo4 + kStripP + 3) / 4;
       if (nq > kStripNQ) return false;
-      need_r = std::max(need_r, kStripP + lo4 + 4 * kStripNQ);  // every band reads the whole strip
+      // the kernel always loads kStripNQ float4 per strip; rows past the group's range may run into the
+      // next window column or past the slot (into the next slot or the staging area): never used
+      need_r = std::max(need_r, kStripP + lo4 + 4 * nq);
       if (box_r) {
         out[e + 0] = (uint32_t)(4LL * (lo4 + (long long)box_r * ccol));
         uint32_t opack = 0;
@@ -1337,8 +1339,11 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
     if (pg.strip) {  // warp-specialised strip forward: one CTA per SM, consumer warps + a producer warp
       nthreads = 32 * (pg.strip_warps + 1);
       // [ring][staging, 1024-byte aligned][mbarriers]; + 1 KB alignment slack of the dynamic base
-      nsmem = ((size_t)128 + kStripStages * slot * sizeof(float) + 1023) / 1024 * 1024 + 1024 +
-              (size_t)pg.strip_warps * kStripStage * sizeof(float);
+      const size_t stage_b = (size_t)pg.strip_warps * kStripStage * sizeof(float);
+      const size_t avail = 227 * 1024 - stage_b - 2048 - 128;
+      A.stages = (int)std::min<size_t>(kStripStagesMax, avail / ((size_t)slot * sizeof(float)));
+      if (const char* e = std::getenv("CTIS_STRIP_STAGES")) A.stages = std::max(2, std::min(A.stages, std::atoi(e)));
+      nsmem = ((size_t)128 + (size_t)A.stages * slot * sizeof(float) + 1023) / 1024 * 1024 + 1024 + stage_b;
       grid = dim3((unsigned)std::min<long long>(items, (long long)P.sms), 1, 1);
     }
     void* args[] = {&A, &tm, &tg};

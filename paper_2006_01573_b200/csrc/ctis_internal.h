@@ -83,7 +83,7 @@ constexpr int kStripMG = 4;   // modes per strip group (accumulators: kStripMG x
 constexpr int kStripNQ = 10;  // max float4 loads per strip (40 window rows)
 constexpr int kStripNO = 4 * kStripNQ - kStripP + 1;  // row offsets 0..24 (one code block per offset)
 constexpr int kStripWarpsMax = 14;  // consumer warps per CTA (+ 1 TMA producer warp): <= 136 registers
-constexpr int kStripStages = 6;
+constexpr int kStripStagesMax = 8;  // ring depth: as many window slots as shared memory holds (<= 8)
 constexpr int kStripStage = kStripMG * 512;  // flush staging floats per warp (kStripMG tiles of 16 x 32)
 
 // Per-launch parameters of the table kernels.
@@ -115,6 +115,7 @@ struct TabArgs {
   // strip forward: flush accumulator tiles with TMA bulk reduce-add through the g_hat tensor map
   // (nowrap plans with 16-byte FPA column strides); otherwise red.global.add with modular indices
   int tma_flush;
+  int stages;          // strip forward: window ring depth (<= kStripStagesMax)
 };
 
 }  // namespace ctis

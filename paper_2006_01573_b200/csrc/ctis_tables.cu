@@ -1016,7 +1016,7 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
 // group reads its kStripP operands from that strip at its own row offset o: the offset is a run-time
 // value, so each (mode slot, o) pair is its own straight-line block (FFMA2 for even o) selected by a
 // warp-uniform switch.  Warp specialisation: the last warp's lane 0 produces the TMA windows into a
-// kStripStages ring (full / empty mbarriers), the consumer warps release a slot as soon as their strip
+// A.stages-deep ring (full / empty mbarriers), the consumer warps release a slot as soon as their strip
 // is in registers.
 #include "ctis_strip_dispatch.inc"
 
@@ -1054,7 +1054,7 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
 template <int MG>
 __device__ __forceinline__ void forward_strip(const TabArgs& A, const CUtensorMap* tm, const CUtensorMap* tg) {
   extern __shared__ __align__(1024) float smem[];
-  constexpr int S = kStripStages;
+  const unsigned S = (unsigned)A.stages;
   static_assert(MG == kStripMG, "descriptor layout assumes kStripMG slots per group");
   const int nch = tabi(0);
   const int per_frame = tabi(kItemBase + nch);
@@ -1068,12 +1068,12 @@ __device__ __forceinline__ void forward_strip(const TabArgs& A, const CUtensorMa
   const unsigned slot_bytes = 4u * A.slot_floats;
   // [full S][empty S] mbarriers | ring: S slots from byte 128 | staging: 1024-byte aligned, kStripStage
   // floats per consumer warp.  Every address is uniform (no per-band rematerialisation from blockDim).
-  const unsigned full = smem0, empty = smem0 + 8 * S;
+  const unsigned full = smem0, empty = smem0 + 8 * kStripStagesMax;
   const unsigned sbase = smem0 + 128;
   const unsigned stage0 = (sbase + S * slot_bytes + 1023u) & ~1023u;
-  static_assert(16 * S <= 128, "mbarriers fit below the ring");
+  static_assert(16 * kStripStagesMax <= 128, "mbarriers fit below the ring");
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
+    for (unsigned s = 0; s < S; ++s) {
       mbar_init(full + 8 * s, 1);
       mbar_init(empty + 8 * s, (unsigned)nwc);
     }
@@ -1093,11 +1093,11 @@ __device__ __forceinline__ void forward_strip(const TabArgs& A, const CUtensorMa
         const uint32_t BI = D + kDescHeader + MG * nhg;
 #pragma unroll 1
         for (int b = 0; b < nb; ++b, ++w) {
-          if (w >= (unsigned)S) mbar_wait(empty + 8 * slot, phase ^ 1u);  // consumers released the slot
+          if (w >= S) mbar_wait(empty + 8 * slot, phase ^ 1u);  // consumers released the slot
           mbar_expect_tx(full + 8 * slot, A.box_bytes);
           tma_4d(sbase + slot * slot_bytes, tm, U_r + tabi(BI + 4 * b), U_c + tabi(BI + 4 * b + 1), lam0 + b, z,
                  full + 8 * slot);
-          if (++slot == (unsigned)S) {
+          if (++slot == S) {
             slot = 0;
             phase ^= 1u;
           }
@@ -1119,7 +1119,8 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
                                                       int per_frame, int nch, int items, unsigned sbase,
                                                       unsigned slot_bytes, unsigned full, unsigned empty,
                                                       unsigned stage) {
-  constexpr int S = kStripStages, NV = 4 * kStripNQ;
+  const unsigned S = (unsigned)A.stages;
+  constexpr int NV = 4 * kStripNQ;
   // ---- consumers: lane = rs + 2*col owns rows 16*rs .. 16*rs+15 of u column col of the 32 x 16 tile
   const int rs = lane & 1, col = lane >> 1;
   unsigned tb = sbase + 4u * (kStripP * rs + A.box_r * col);
@@ -1168,7 +1169,7 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
       if (act) strip_load(v, tslot + c0.x);
       if (elect_one()) mbar_arrive(empty + 8 * slot);  // the strip is in registers: the slot may be refilled
       tslot += slot_bytes;
-      if (++slot == (unsigned)S) {
+      if (++slot == S) {
         slot = 0;
         phase ^= 1u;
         tslot = tb;
@@ -1345,6 +1346,6 @@ extern "C" __global__ void __launch_bounds__(32 * (kStripWarpsMax + 1), 1)
     ctis_fwd_strip_t(const TabArgs A, const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tg) {
   if (A.frames == 0) return;
   pdl_enter();
-  if (A.dbg & 8) nan_fill_smem(kStripStages * A.slot_floats);
+  if (A.dbg & 8) nan_fill_smem(32 + A.stages * A.slot_floats);
   forward_strip<kStripMG>(A, &tm, &tg);
 }
