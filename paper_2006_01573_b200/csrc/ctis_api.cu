@@ -1493,6 +1493,8 @@ ctis_status run_mlem(ctis_plan_s& P, const float* g, float* f, int64_t frames, i
     e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
+    e = cudaGraphUpload(exec, P.side);  // device-side setup now, not inside the first timed launch
+    if (e != cudaSuccess) return cuda_fail(e, "graph upload");
     it = P.graphs.emplace(key, exec).first;
     P.graph_launches[key] = cnt;
   } else {

@@ -14,8 +14,8 @@ solver = sys.argv[3] if len(sys.argv) > 3 else "mlem"   # mlem | monitored | sma
 cfg = syn.config(name)
 plan = ctis.Plan.from_geometry(cfg.geom, syn.paper_taps(cfg))
 plan.set_option(ctis.OPT_VALIDATE_DATA, 0)
-if os.environ.get("CTIS_FUSED") == "0":
-    plan.set_option(ctis.OPT_FUSED_RATIO, 0)
+if os.environ.get("CTIS_FUSED") is not None:
+    plan.set_option(ctis.OPT_FUSED_RATIO, int(os.environ["CTIS_FUSED"]))
 g = plan.forward(torch.from_numpy(syn.scene_blobs(cfg.geom).reshape(-1)).cuda())
 f = torch.ones(cfg.geom.m, device="cuda")
 def run():
