@@ -110,6 +110,11 @@ struct ctis_plan_s {
   int a = 0, alpha = 0, w = 0, gamma = 0, xi = 0, n = 0, ell = 0, m = 0;
   int64_t band_begin = 0, band_end = 0, total_taps = 0;
   int64_t ex_lo = 0, ex_hi = 0;  // FPA index range any tap of any band reaches (latency-mode exchange)
+  // Reachable FPA box of a no-wrap plan (every tap a 2-D translation): pixel rows [rb_r0, rb_r0 + 4*rb_nr4)
+  // x columns [rb_c0, rb_c0 + rb_nc) hold every pixel E(q) + o of every voxel and tap; outside it g_hat
+  // is identically 0, r is 0 (reading R4) and no back projection reads r, so the MLEM ratio pass only
+  // runs over the box (rb_nr4 = 0: the whole FPA)
+  int rb_r0 = 0, rb_nr4 = 0, rb_c0 = 0, rb_nc = 0;
   bool shard = false, validate = true, use_graph = true;
   bool tma_f = false, tma_b = false;
   int back_nb = kBackBandsMax;
@@ -117,6 +122,12 @@ struct ctis_plan_s {
   int fbox_r = 0, fbox_c = 0, bbox_r = 0, bbox_c = 0;
   int fwd_g = 1, fwd_m = 8;
   bool fwd_strip = false;  // forward pages use the strip kernel (ctis_tables.cu forward_strip)
+  // TMA forward with a field stop whose rows are not a multiple of 4 floats (a % 4 != 0, e.g. the paper's
+  // own 89 x 80): f is repacked into d_fpad with a 16-byte row pitch f_pitch = round4(a) before
+  // each forward launch (the TMA view keeps dims a x alpha, so the pad rows are never read)
+  int f_pitch = 0;
+  float* d_fpad = nullptr;
+  size_t fpad_cap = 0;  // floats
   int sms = 148;
   bool pair = false;  // FFMA2 on tap pairs (16-byte entries) or plain FFMA (8-byte entries)
   bool nowrap = false;  // no tap carries across FPA columns or wraps past n (2-D translations only)
@@ -162,7 +173,7 @@ struct ctis_plan_s {
     for (auto* pages : {&fwd, &back})
       for (Page& p : *pages)
         if (p.lib) cudaLibraryUnload(p.lib);
-    for (void* p : {(void*)d_hband, (void*)d_flag, (void*)d_g, (void*)d_f, d_ws, (void*)d_gbar})
+    for (void* p : {(void*)d_hband, (void*)d_flag, (void*)d_g, (void*)d_f, d_ws, (void*)d_gbar, (void*)d_fpad})
       if (p) cudaFree(p);
   }
 };
@@ -778,7 +789,13 @@ int choose_back_nb(const ctis_plan_s& P) {
 ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& bands, const std::vector<float>& invh) {
   // TMA needs 16-byte global strides: a % 4 == 0 for f, gamma % 4 == 0 for r.
   P.pair = true;  // FFMA2 on tap pairs (plain FFMA measured no faster on B200)
-  P.tma_f = (P.a % 4 == 0);
+  // TMA forward: f rows need a 16-byte pitch — a % 4 == 0, or a repacked copy (f_pitch; CTIS_FWD_REPACK=0
+  // keeps the element-loader forward for such plans)
+  P.f_pitch = (P.a + 3) / 4 * 4;
+  {
+    const char* e = std::getenv("CTIS_FWD_REPACK");
+    P.tma_f = (P.a % 4 == 0) || !(e && std::atoi(e) == 0);
+  }
   P.nowrap = true;
   for (const auto& b : bands)
     for (const TapXY& t : b)
@@ -1037,6 +1054,17 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
       ex_hi = n - 1;
     }
   }
+  // reachable 2-D box (no-wrap taps of this plan's bands only)
+  int64_t br0 = gamma, br1 = -1, bc0 = xi, bc1 = -1;
+  bool box_ok = gamma % 4 == 0;
+  for (int64_t t = tap_ptr[b0]; t < tap_ptr[b1] && box_ok; ++t) {
+    const int64_t dr = tap_offset[t] % gamma, dc = tap_offset[t] / gamma;
+    if (dr > gamma - a || dc > xi - alpha) box_ok = false;  // carries across columns / wraps (Eq. 7)
+    br0 = std::min(br0, dr);
+    br1 = std::max(br1, dr + a - 1);
+    bc0 = std::min(bc0, dc);
+    bc1 = std::max(bc1, dc + alpha - 1);
+  }
   int ndev = 0;
   CTIS_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
   if (device < 0 || device >= ndev) return fail(CTIS_ERR_INVALID_ARGUMENT, "device ordinal out of range");
@@ -1053,6 +1081,15 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
   p->band_end = b1;
   p->ex_lo = ex_lo;
   p->ex_hi = ex_hi;
+  // (only when the box saves >= 10 % of the FPA: C4's box is the whole FPA and the per-element index
+  // arithmetic then costs 0.4 us per iteration; the paper's 89 x 80 field stop reaches ~1/3)
+  if (box_ok && br1 >= br0 && !std::getenv("CTIS_NO_RATIO_BOX") &&
+      ((br1 + 1 - (br0 & ~int64_t(3)) + 3) / 4 * 4) * (bc1 + 1 - bc0) * 10 < 9 * n) {
+    p->rb_r0 = (int)(br0 & ~int64_t(3));
+    p->rb_nr4 = (int)((br1 + 1 - p->rb_r0 + 3) / 4);
+    p->rb_c0 = (int)bc0;
+    p->rb_nc = (int)(bc1 + 1 - bc0);
+  }
   p->a = (int)a;
   p->alpha = (int)alpha;
   p->w = (int)(b1 - b0);
@@ -1200,7 +1237,8 @@ cudaError_t make_tensor_map(CUtensorMap* tm, bool forward, const ctis_plan_s& P,
   CUresult r;
   if (forward) {
     const cuuint64_t dims[4] = {(cuuint64_t)P.a, (cuuint64_t)P.alpha, (cuuint64_t)P.w, (cuuint64_t)frames};
-    const cuuint64_t strides[3] = {4ull * P.a, 4ull * P.ell, 4ull * P.m};
+    const cuuint64_t pitch = (cuuint64_t)P.f_pitch;  // == a unless f was repacked (d_fpad)
+    const cuuint64_t strides[3] = {4ull * pitch, 4ull * pitch * P.alpha, 4ull * pitch * P.alpha * P.w};
     // CTIS_DEBUG & 32 (profiling only, results invalid): half-width boxes, to measure what smaller
     // per-band windows would save in TMA traffic
     const cuuint32_t bc = (debug_flags() & 32) ? (cuuint32_t)std::max(1, P.fbox_c / 2) : (cuuint32_t)P.fbox_c;
@@ -1270,6 +1308,30 @@ struct Fuse {
 };
 
 
+// Repack buffer for plans with f_pitch != a: allocated outside stream capture (entry points call this
+// before capturing; inside a capture an undersized buffer is an error, never an allocation).
+cudaError_t ensure_fpad(ctis_plan_s& P, int frames, cudaStream_t s) {
+  if (P.f_pitch == P.a) return cudaSuccess;
+  const size_t need = (size_t)P.f_pitch * P.alpha * P.w * (size_t)frames;
+  if (need <= P.fpad_cap) return cudaSuccess;
+  if (s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(s, &cs);
+    if (e != cudaSuccess) return e;
+    if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;
+  }
+  if (P.d_fpad) {
+    cudaError_t e = cudaDeviceSynchronize();  // the old buffer may still be read by queued launches
+    if (e != cudaSuccess) return e;
+    cudaFree(P.d_fpad);
+    P.d_fpad = nullptr;
+    P.fpad_cap = 0;
+  }
+  cudaError_t e = cudaMalloc(&P.d_fpad, need * sizeof(float));
+  if (e == cudaSuccess) P.fpad_cap = need;
+  return e;
+}
+
 cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const float* src, float* dst,
                          long long src_frame, long long dst_frame, int frames, int mode, cudaStream_t s,
                          int64_t* count, const Fuse* fuse = nullptr) {
@@ -1292,6 +1354,14 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
   alignas(64) CUtensorMap tm, tg;
   std::memset(&tm, 0, sizeof(tm));
   std::memset(&tg, 0, sizeof(tg));
+  if (tma && fwd && P.f_pitch != P.a) {  // repack f to the 16-byte row pitch of the TMA view
+    cudaError_t e = ensure_fpad(P, frames, s);
+    if (e != cudaSuccess) return e;
+    e = launch_repack_rows(src, P.d_fpad, P.a, P.f_pitch, (long long)P.alpha * P.w * frames, s);
+    if (e != cudaSuccess) return e;
+    if (count) ++*count;
+    src = P.d_fpad;
+  }
   if (tma) {
     cudaError_t e = make_tensor_map(&tm, fwd, P, src, frames);
     if (e != cudaSuccess) return e;
@@ -1436,8 +1506,12 @@ cudaError_t enqueue_mlem(ctis_plan_s& P, const float* g, float* f, float* ws, in
   for (int k = 0; k < iters && e == cudaSuccess; ++k) {
     e = enqueue_forward(P, f, A, frames, s, cnt);
     if (e == cudaSuccess) {
-      e = solver == 1 ? launch_log_ratio(g, A, B, count, s, pdl_enabled())
-                      : launch_ratio(g, A, B, count, /*zero_ghat=*/true, s, pdl_enabled());
+      if (solver == 1)
+        e = launch_log_ratio(g, A, B, count, s, pdl_enabled());
+      else if (P.rb_nr4 > 0 && P.projector == 0)  // only the reachable FPA box (ctis_plan_s::rb_*)
+        e = launch_ratio_box(g, A, B, P.n, P.gamma, P.rb_r0, P.rb_nr4, P.rb_c0, P.rb_nc, frames, s, pdl_enabled());
+      else
+        e = launch_ratio(g, A, B, count, /*zero_ghat=*/true, s, pdl_enabled());
       ++*cnt;
     }
     if (e == cudaSuccess) e = enqueue_back(P, B, f, frames, solver == 1 ? 2 : 1, s, cnt);
@@ -1460,6 +1534,7 @@ ctis_status run_mlem(ctis_plan_s& P, const float* g, float* f, int64_t frames, i
   if (st) return st;
   if ((st = check_ptrs({g, f, ws}))) return st;
   DeviceGuard dg(P.device);
+  CTIS_CUDA(ensure_fpad(P, (int)frames, nullptr), "f repack buffer");  // before any stream capture
   P.last_launches = 0;
   if (P.validate) {
     if ((st = validate_data(P, g, f, frames, s))) return st;
@@ -1522,6 +1597,7 @@ ctis_status run_mlem_monitored(ctis_plan_s& P, const float* g, float* f, int max
   if (!ll || !cnt || (reinterpret_cast<uintptr_t>(ll) & 7u) || (reinterpret_cast<uintptr_t>(cnt) & 3u))
     return fail(CTIS_ERR_INVALID_ARGUMENT, "ll (8-byte aligned) and iters_done (4-byte aligned) must be device pointers");
   DeviceGuard dg(P.device);
+  CTIS_CUDA(ensure_fpad(P, (int)1, nullptr), "f repack buffer");  // before any stream capture
   P.last_launches = 0;
   if (P.validate) {
     if ((st = validate_data(P, g, f, 1, s))) return st;
@@ -1660,6 +1736,7 @@ ctis_status run_band_sharded(ctis_plan_s& P, ctis_comm_s& C, const float* g, flo
   ctis_status st = check_ptrs({g, f, ws});
   if (st) return st;
   DeviceGuard dg(P.device);
+  CTIS_CUDA(ensure_fpad(P, (int)1, nullptr), "f repack buffer");  // before any stream capture
   P.last_launches = 0;
   if (iters == 0) return CTIS_OK;
   float* X = static_cast<float*>(ws);

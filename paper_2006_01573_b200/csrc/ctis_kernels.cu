@@ -66,6 +66,55 @@ cudaError_t launch_ratio(const float* g, float* ghat, float* r, long long count,
   return launch_ex(ratio_kernel, blocks, 256, s, pdl, g, ghat, r, count, zero_ghat ? 1 : 0);
 }
 
+// Ratio over the reachable pixel box of each frame: float4 i of the box is rows
+// r0 + 4*(i % nr4) .. +3 of column c0 + (i / nr4) % nc of frame i / (nr4 * nc); g_hat is reset to 0.
+__global__ void ratio_box_kernel(const float* __restrict__ g, float* gh, float* r, long long n, int gamma, int r0,
+                                 int nr4, int c0, int nc, long long total4) {
+  pdl_enter();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long per_frame = (long long)nr4 * nc;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total4; i += stride) {
+    const long long z = i / per_frame;
+    const long long k = i - z * per_frame;
+    const long long col = k / nr4;
+    const long long p = z * n + (c0 + col) * (long long)gamma + r0 + 4 * (k - col * nr4);
+    const float4 gv = __ldg(reinterpret_cast<const float4*>(g + p));
+    const float4 hv = *reinterpret_cast<const float4*>(gh + p);
+    float4 o;
+    o.x = hv.x > 0.f ? __fdiv_rn(gv.x, hv.x) : 0.f;
+    o.y = hv.y > 0.f ? __fdiv_rn(gv.y, hv.y) : 0.f;
+    o.z = hv.z > 0.f ? __fdiv_rn(gv.z, hv.z) : 0.f;
+    o.w = hv.w > 0.f ? __fdiv_rn(gv.w, hv.w) : 0.f;
+    *reinterpret_cast<float4*>(r + p) = o;
+    *reinterpret_cast<float4*>(gh + p) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+cudaError_t launch_ratio_box(const float* g, float* ghat, float* r, long long n, int gamma, int r0, int nr4, int c0,
+                             int nc, int frames, cudaStream_t s, bool pdl) {
+  const long long total4 = (long long)nr4 * nc * frames;
+  const long long want = (total4 + 255) / 256;
+  const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
+  return launch_ex(ratio_box_kernel, blocks, 256, s, pdl, g, ghat, r, n, gamma, r0, nr4, c0, nc, total4);
+}
+
+// Row repack of f for the TMA forward (plans with a % 4 != 0): one thread per element.
+__global__ void repack_rows_kernel(const float* __restrict__ src, float* __restrict__ dst, int a, int pitch,
+                                   long long total) {
+  pdl_enter();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long c = i / a;
+    dst[c * pitch + (i - c * a)] = __ldg(src + i);
+  }
+}
+
+cudaError_t launch_repack_rows(const float* src, float* dst, int a, int pitch, long long cols, cudaStream_t s) {
+  const long long total = (long long)a * cols;
+  const long long want = (total + 255) / 256;
+  const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
+  return launch_ex(repack_rows_kernel, blocks, 256, s, false, src, dst, a, pitch, total);
+}
+
 __global__ void sensitivity_kernel(const float* __restrict__ hband, float* __restrict__ h, int ell, int m) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) h[j] = __ldg(hband + j / ell);
 }

@@ -7,6 +7,12 @@ namespace ctis {
 // pdl: launch with programmatic stream serialization (the kernels call griddepcontrol.wait first)
 cudaError_t launch_ratio(const float* g, float* ghat, float* r, long long count, bool zero_ghat, cudaStream_t s,
                          bool pdl = false);
+// ratio (zeroing g_hat) over the pixel box rows [r0, r0 + 4*nr4) x columns [c0, c0 + nc) of every frame
+// (frames of n pixels, column pitch gamma; r0 and gamma multiples of 4, buffers 16-byte aligned)
+cudaError_t launch_ratio_box(const float* g, float* ghat, float* r, long long n, int gamma, int r0, int nr4, int c0,
+                             int nc, int frames, cudaStream_t s, bool pdl = false);
+// dst[c * pitch + r] = src[c * a + r] for r < a, c < cols (row repack to a 16-byte pitch for TMA)
+cudaError_t launch_repack_rows(const float* src, float* dst, int a, int pitch, long long cols, cudaStream_t s);
 cudaError_t launch_sensitivity(const float* hband, float* h, int ell, int m, cudaStream_t s);
 cudaError_t launch_validate(const float* x, long long count, int* flag, cudaStream_t s);
 // SMART log-ratio (zeroing g_hat)

@@ -489,17 +489,45 @@ def test_error_codes(ctis, dev):
     assert ei.value.status == ctis.ERR_INVALID_ARGUMENT
 
 
-def test_no_stale_shared_memory_reads(ctis):
+@pytest.mark.parametrize("variant", ["default", "loader", "strip"])
+def test_no_stale_shared_memory_reads(ctis, variant):
     """Every projection kernel with CTIS_DEBUG=8 NaN-fills its window ring first: results must not
-    change (a band without taps in a forward pass once read a slot it never loaded)."""
+    change (a band without taps in a forward pass once read a slot it never loaded).  Variants: the
+    default kernel choice (odd field stops take the repacked TMA forward), the element-loader forward
+    (CTIS_FWD_REPACK=0) and the strip forward forced on every TMA plan (CTIS_FWD_STRIP=1)."""
     import os
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     env = dict(os.environ, CTIS_DEBUG="8")
-    r = subprocess.run([sys.executable, os.path.join(here, "poison_case.py")], env=env, capture_output=True,
-                       text=True, timeout=600)
+    if variant == "loader":
+        env["CTIS_FWD_REPACK"] = "0"
+    if variant == "strip":
+        env["CTIS_FWD_STRIP"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(here, "poison_case.py"), "solvers"], env=env,
+                       capture_output=True, text=True, timeout=900)
+    print(r.stdout[-2000:])
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("name", ["T1w3", "T1w24"])
+def test_paper_table1_geometry_vs_oracle(ctis, oracle_lib, dev, name):
+    """The paper's own benchmark geometry (89 x 80 field stop on a 2048^2 FPA, w = 3 / 24): the odd
+    field stop (a % 4 != 0) runs the repacked TMA forward and the reachable-box ratio pass.  Single
+    projections at 1e-5 and MLEM K = 25 (Table 1's K) at 1e-3 against the oracle."""
+    cfg = syn.config(name)
+    geom, taps = cfg.geom, syn.paper_taps(cfg)
+    plan = ctis.Plan.from_geometry(geom, taps)
+    ft = syn.scene_constant(geom)                       # P:221: fully illuminated field stop, f = 100
+    g_np = oracle_lib.forward(geom, taps, ft).astype(np.float32)
+    check(plan.forward(cuda(ft.ravel(), dev)).cpu().numpy(), oracle_lib.forward(geom, taps, ft), PROJ_TOL,
+          f"{name} forward")
+    u = np.random.default_rng(5).uniform(0.5, 1.5, geom.n).astype(np.float32)
+    check(plan.backproject(cuda(u, dev)).cpu().numpy(), oracle_lib.backproject(geom, taps, u), PROJ_TOL,
+          f"{name} back")
+    f = torch.ones(geom.m, device=dev)
+    plan.mlem(cuda(g_np, dev), f, cfg.K)
+    check(f.cpu().numpy(), oracle_lib.mlem(geom, taps, g_np, np.ones(geom.m), cfg.K), MLEM_TOL, f"{name} MLEM K={cfg.K}")
 
 
 # ------------------------------------------------------------------ §8(f) f-3: log-likelihood, early stop, H^T g init
