@@ -128,6 +128,13 @@ struct ctis_plan_s {
   int f_pitch = 0;
   float* d_fpad = nullptr;
   size_t fpad_cap = 0;  // floats
+  // Mode-split back projection for latency-bound small plans (too few tile x band-chunk work items to fill
+  // the SMs): every chunk's modes are cut into back_split descriptors that add their partial z into d_z
+  // (red.add, TabArgs::mode 3); one update pass then applies Eq. 2's multiplicative step and re-zeroes d_z
+  int back_split = 1;
+  float* d_z = nullptr;
+  size_t z_cap = 0;         // floats
+  float* d_invh = nullptr;  // 1/h_lambda (fp32, the epilogue's values) for the update pass
   int sms = 148;
   bool pair = false;  // FFMA2 on tap pairs (16-byte entries) or plain FFMA (8-byte entries)
   bool nowrap = false;  // no tap carries across FPA columns or wraps past n (2-D translations only)
@@ -173,7 +180,7 @@ struct ctis_plan_s {
     for (auto* pages : {&fwd, &back})
       for (Page& p : *pages)
         if (p.lib) cudaLibraryUnload(p.lib);
-    for (void* p : {(void*)d_hband, (void*)d_flag, (void*)d_g, (void*)d_f, d_ws, (void*)d_gbar, (void*)d_fpad})
+    for (void* p : {(void*)d_hband, (void*)d_flag, (void*)d_g, (void*)d_f, d_ws, (void*)d_gbar, (void*)d_fpad, (void*)d_z, (void*)d_invh})
       if (p) cudaFree(p);
   }
 };
@@ -985,6 +992,46 @@ ctis_status build_tables(ctis_plan_s& P, const std::vector<std::vector<TapXY>>& 
       descs.push_back(std::move(d));
       tiles.push_back(t);
     }
+    // Mode split (single-frame layouts with fewer work items than CTA slots, persistent TMA kernels):
+    // re-emit every chunk as S descriptors over consecutive subsets of its modes
+    P.back_split = 1;
+    if (P.tma_b && !P.throughput && !P.shard) {
+      long long items = 0;
+      for (int t : tiles) items += t;
+      // as many subsets as still fit ONE wave of CTA slots (2 per SM): a second wave costs a whole item's
+      // latency again (measured: C3 2 subsets = 416 items, back 25 -> 50 us; T1w3 8 subsets, 22 vs 40 us)
+      // only for plans that leave most SMs idle (< 1 item per 2 SMs): C2 (2 subsets) and T1w24 measured
+      // slower split (18.9 vs 17.4 us per MLEM iteration), T1w3 (30 items, 8 subsets) 36.3 -> 18.1 us
+      int S = items * 2 <= P.sms ? (int)std::min<long long>(8, (2LL * P.sms) / std::max<long long>(1, items)) : 1;
+      if (const char* e = std::getenv("CTIS_BACK_SPLIT")) S = std::max(1, std::min(8, std::atoi(e)));
+      size_t nm_min = SIZE_MAX;
+      for (const auto& ms : cms) nm_min = std::min(nm_min, ms.size());
+      S = (int)std::min<size_t>((size_t)S, std::max<size_t>(1, nm_min / 4));
+      if (S > 1 && descs.size() == todo.size()) {
+        std::vector<std::vector<uint32_t>> sd;
+        std::vector<int> st;
+        bool ok = true;
+        for (size_t k = 0; k < todo.size() && ok; ++k) {
+          const int b0 = todo[k].first, nb = todo[k].second;
+          const size_t nm = cms[k].size();
+          for (int j = 0; j < S && ok; ++j) {
+            const size_t c0 = nm * j / S, c1 = nm * (j + 1) / S;
+            if (c1 <= c0) continue;
+            std::vector<Mode> sub(cms[k].begin() + (long)c0, cms[k].begin() + (long)c1);
+            std::vector<uint32_t> d;
+            int t = 0;
+            ok = back_desc(P, b0, nb, P.back_nb, sub, invh, box_r, box_c, d, t);
+            sd.push_back(std::move(d));
+            st.push_back(t);
+          }
+        }
+        if (ok) {
+          descs.swap(sd);
+          tiles.swap(st);
+          P.back_split = S;
+        }
+      }
+    }
     std::vector<int> nbs(descs.size(), P.back_nb);  // back pages: "max_modes" carries NB
     pack_pages(P.back, false, descs, tiles, nbs);
   }
@@ -1116,6 +1163,11 @@ ctis_status build_plan(int64_t a, int64_t alpha, int64_t w, int64_t gamma, int64
     p->total_taps += (int64_t)bt.size();
   }
   p->inv_h = invh;
+  if (cudaMalloc(&p->d_invh, sizeof(float) * p->w) != cudaSuccess ||
+      cudaMemcpy(p->d_invh, invh.data(), sizeof(float) * p->w, cudaMemcpyHostToDevice) != cudaSuccess) {
+    delete p;
+    return fail(CTIS_ERR_OUT_OF_MEMORY, "1/h upload");
+  }
   p->throughput = throughput;
   ctis_status st = build_tables(*p, bands, invh);
   cudaError_t e = cudaSuccess;
@@ -1332,6 +1384,29 @@ cudaError_t ensure_fpad(ctis_plan_s& P, int frames, cudaStream_t s) {
   return e;
 }
 
+// Partial-z buffer of mode-split plans: allocated zeroed outside stream capture; the update pass keeps it
+// zero between uses.
+cudaError_t ensure_z(ctis_plan_s& P, int frames, cudaStream_t s) {
+  if (P.back_split <= 1) return cudaSuccess;
+  const size_t need = (size_t)P.m * (size_t)frames;
+  if (need <= P.z_cap) return cudaSuccess;
+  if (s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(s, &cs);
+    if (e != cudaSuccess) return e;
+    if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return e;
+  if (P.d_z) cudaFree(P.d_z);
+  P.d_z = nullptr;
+  P.z_cap = 0;
+  e = cudaMalloc(&P.d_z, need * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemset(P.d_z, 0, need * sizeof(float));
+  if (e == cudaSuccess) P.z_cap = need;
+  return e;
+}
+
 cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const float* src, float* dst,
                          long long src_frame, long long dst_frame, int frames, int mode, cudaStream_t s,
                          int64_t* count, const Fuse* fuse = nullptr) {
@@ -1446,6 +1521,21 @@ cudaError_t enqueue_back(ctis_plan_s& P, const float* r, float* fz, int frames, 
     }
     return cudaSuccess;
   }
+  if (P.back_split > 1) {  // mode split: partial z of every mode subset accumulated with red.add
+    const size_t count = (size_t)P.m * frames;
+    if (mode == 0) {  // z = H^T r straight into the caller's buffer
+      cudaError_t e = cudaMemsetAsync(fz, 0, sizeof(float) * count, s);
+      if (e != cudaSuccess) return e;
+      return launch_pages(P, P.back, r, fz, P.n, P.m, frames, 3, s, cnt, fuse);
+    }
+    cudaError_t e = ensure_z(P, frames, s);
+    if (e != cudaSuccess) return e;
+    e = launch_pages(P, P.back, r, P.d_z, P.n, P.m, frames, 3, s, cnt, fuse);
+    if (e != cudaSuccess) return e;
+    e = launch_split_update(fz, P.d_z, P.d_invh, P.ell, P.w, (long long)count, mode, s);
+    if (cnt) ++*cnt;
+    return e;
+  }
   return launch_pages(P, P.back, r, fz, P.n, P.m, frames, mode, s, cnt, fuse);
 }
 
@@ -1535,6 +1625,7 @@ ctis_status run_mlem(ctis_plan_s& P, const float* g, float* f, int64_t frames, i
   if ((st = check_ptrs({g, f, ws}))) return st;
   DeviceGuard dg(P.device);
   CTIS_CUDA(ensure_fpad(P, (int)frames, nullptr), "f repack buffer");  // before any stream capture
+  CTIS_CUDA(ensure_z(P, (int)frames, nullptr), "partial z buffer");
   P.last_launches = 0;
   if (P.validate) {
     if ((st = validate_data(P, g, f, frames, s))) return st;
@@ -1598,6 +1689,7 @@ ctis_status run_mlem_monitored(ctis_plan_s& P, const float* g, float* f, int max
     return fail(CTIS_ERR_INVALID_ARGUMENT, "ll (8-byte aligned) and iters_done (4-byte aligned) must be device pointers");
   DeviceGuard dg(P.device);
   CTIS_CUDA(ensure_fpad(P, (int)1, nullptr), "f repack buffer");  // before any stream capture
+  CTIS_CUDA(ensure_z(P, 1, nullptr), "partial z buffer");
   P.last_launches = 0;
   if (P.validate) {
     if ((st = validate_data(P, g, f, 1, s))) return st;
@@ -1737,6 +1829,7 @@ ctis_status run_band_sharded(ctis_plan_s& P, ctis_comm_s& C, const float* g, flo
   if (st) return st;
   DeviceGuard dg(P.device);
   CTIS_CUDA(ensure_fpad(P, (int)1, nullptr), "f repack buffer");  // before any stream capture
+  CTIS_CUDA(ensure_z(P, 1, nullptr), "partial z buffer");
   P.last_launches = 0;
   if (iters == 0) return CTIS_OK;
   float* X = static_cast<float*>(ws);

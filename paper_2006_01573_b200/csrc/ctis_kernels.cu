@@ -115,6 +115,27 @@ cudaError_t launch_repack_rows(const float* src, float* dst, int a, int pitch, l
   return launch_ex(repack_rows_kernel, blocks, 256, s, false, src, dst, a, pitch, total);
 }
 
+// Update pass of mode-split back projections (ctis_api.cu enqueue_back): the epilogue's arithmetic
+// (ctis_tables.cu upd_value) on the accumulated z, which is re-zeroed for the next accumulation.
+__global__ void split_update_kernel(float* f, float* z, const float* __restrict__ invh, int ell, int w,
+                                    long long count, int mode) {
+  pdl_enter();
+  const long long m = (long long)ell * w;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < count; j += (long long)gridDim.x * blockDim.x) {
+    const float ih = __ldg(invh + (j % m) / ell);
+    const float zz = z[j];
+    z[j] = 0.f;
+    f[j] = mode == 1 ? f[j] * zz * ih : mode == 2 ? f[j] * expf(zz * ih) : zz;
+  }
+}
+
+cudaError_t launch_split_update(float* f, float* z, const float* invh, int ell, int w, long long count, int mode,
+                                cudaStream_t s) {
+  const long long want = (count + 255) / 256;
+  const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
+  return launch_ex(split_update_kernel, blocks, 256, s, false, f, z, invh, ell, w, count, mode);
+}
+
 __global__ void sensitivity_kernel(const float* __restrict__ hband, float* __restrict__ h, int ell, int m) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) h[j] = __ldg(hband + j / ell);
 }

@@ -13,6 +13,10 @@ cudaError_t launch_ratio_box(const float* g, float* ghat, float* r, long long n,
                              int nc, int frames, cudaStream_t s, bool pdl = false);
 // dst[c * pitch + r] = src[c * a + r] for r < a, c < cols (row repack to a 16-byte pitch for TMA)
 cudaError_t launch_repack_rows(const float* src, float* dst, int a, int pitch, long long cols, cudaStream_t s);
+// mode-split back update: f[j] <- upd(mode, f[j], z[j], invh[(j % (ell*w)) / ell]) (1: f*z*ih, 2: f*exp(z*ih)),
+// z[j] <- 0, for j < count (frames of ell*w voxels)
+cudaError_t launch_split_update(float* f, float* z, const float* invh, int ell, int w, long long count, int mode,
+                                cudaStream_t s);
 cudaError_t launch_sensitivity(const float* hband, float* h, int ell, int m, cudaStream_t s);
 cudaError_t launch_validate(const float* x, long long count, int* flag, cudaStream_t s);
 // SMART log-ratio (zeroing g_hat)

@@ -64,7 +64,8 @@ __device__ __forceinline__ void cp_wait() {
 __device__ __forceinline__ int tabi(uint32_t i) { return (int)c_tab[i]; }
 
 // Back-projection epilogue (TabArgs::mode): 0 z = H^T r; 1 MLEM f <- f * z / h (Eq. 2, Alg. 1 l. 12);
-// 2 SMART f <- f * exp(z / h) with r the log-ratio (R17)
+// 2 SMART f <- f * exp(z / h) with r the log-ratio (R17); 3 z += partial H^T r (red.add: mode-split
+// plans, the update runs as a separate pass)
 __device__ __forceinline__ float upd_value(int mode, float f, float z, float ih) {
   return mode == 1 ? f * z * ih : mode == 2 ? f * expf(z * ih) : z;
 }
@@ -970,6 +971,21 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
     float* f = A.dst + (long long)z * A.dst_frame;
     const int qr = q_r0 + lane;
     constexpr int EG = NB < 6 ? NB : 6;
+    if (A.mode == 3) {  // mode-split plans: add this mode subset's partial z (ctis_api.cu enqueue_back)
+      if (qr < A.a) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+          if (b < nb) {
+            const long long lb = (long long)(lam0 + b) * A.ell + qr;
+#pragma unroll
+            for (int k4 = 0; k4 < POS; ++k4) {
+              const int qc = q_c0 + warp + NWARPS * k4;
+              if (qc < A.alpha) red_nz(f + lb + (long long)A.a * qc, (b & 1) ? acc[k4][b >> 1].y : acc[k4][b >> 1].x);
+            }
+          }
+      }
+      continue;
+    }
     if (qr < A.a) {
 #pragma unroll
       for (int b0 = 0; b0 < NB; b0 += EG) {
