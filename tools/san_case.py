@@ -35,6 +35,8 @@ def run(geom, taps, frames=1, iters=2, solvers=False):
 
 
 case = sys.argv[1] if len(sys.argv) > 1 else "bench"
+if case == "loader":  # odd field stops otherwise take the repacked TMA forward (which racecheck cannot run)
+    os.environ["CTIS_FWD_REPACK"] = "0"
 if case == "bench":
     for name in ("tiny", "C2"):
         cfg = syn.config(name)
