@@ -1218,9 +1218,14 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
       __syncwarp();
       staged = false;
     }
+    unsigned live = 0;  // modes whose tile holds a nonzero accumulator (dead tiles: u outside the mode's range)
 #pragma unroll
     for (int m = 0; m < MG; ++m) {
       const unsigned tile_s = stage + 2048u * m + 128u * col;
+      bool nz = false;
+#pragma unroll
+      for (int i = 0; i < kStripP; ++i) nz |= acc[m][i] != 0.f;
+      live |= __any_sync(0xffffffffu, nz) ? 1u << m : 0u;
 #pragma unroll
       for (int j = 0; j < kStripP / 4; ++j)
         asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(tile_s + 16u * ((4 * rs + j) ^ (col & 7))),
@@ -1233,7 +1238,7 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
 #pragma unroll 1
     for (int m = 0; m < MG; ++m) {
       const unsigned o = c_tab[D + kDescHeader + MG * warp + m];
-      if (o == 0xffffffffu) continue;
+      if (o == 0xffffffffu || !((live >> m) & 1u)) continue;
       const int r0 = U_r + (int)(o % (unsigned)A.gamma), c0 = U_c + (int)(o / (unsigned)A.gamma);
       const unsigned tile_s = stage + 2048u * m;
       if (tma_flush && r0 >= 0 && (r0 & 3) == 0 && c0 >= 0 && r0 + kFwdTR <= A.gamma && c0 + kFwdTC <= A.xi) {
