@@ -808,7 +808,10 @@ template <int NB, int POS, bool REFILL = CTIS_BACK_REFILL>
 __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtensorMap* tm) {
   constexpr int TC = 8 * POS;
   extern __shared__ __align__(128) float smem[];
-  constexpr int S = kBackStages, K = S / 2, BP = NB / 2;
+#ifndef CTIS_BACK_K
+#define CTIS_BACK_K 6  // measured (B200): K = 2/3/4/6/7 -> C4 back 60.6/59.8/59.8/58.2/59.7 us, C3 29.1/25.1/25.1/23.0 us
+#endif
+  constexpr int S = kBackStages, K = CTIS_BACK_K, BP = NB / 2;  // refill every K windows
   constexpr int NWARPS = kBack4Threads / 32;  // 8: voxel columns warp + 8k, k < 4
   const int nch = tabi(0);
   const int per_frame = tabi(kItemBase + nch);
