@@ -627,7 +627,10 @@ __device__ __forceinline__ void zero_pass(const TabArgs& A) {
 template <int MAXM, int S, bool EARLY, int PROBE = CTIS_FWD_PROBE>
 __device__ __forceinline__ void forward_persistent2(const TabArgs& A, const CUtensorMap* tm) {
   extern __shared__ __align__(128) float smem[];
-  constexpr int K = S / 2, MP = MAXM / 2;
+#ifndef CTIS_FWD_K
+#define CTIS_FWD_K (S / 2)
+#endif
+  constexpr int K = CTIS_FWD_K, MP = MAXM / 2;  // refill every K windows
   constexpr int NW = kFwd2Threads / 32;  // 8 warps; warp w owns columns w and w + NW
   static_assert(2 * NW == kFwdTC, "two columns per warp");
   const int nch = tabi(0);
