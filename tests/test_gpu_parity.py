@@ -489,12 +489,13 @@ def test_error_codes(ctis, dev):
     assert ei.value.status == ctis.ERR_INVALID_ARGUMENT
 
 
-@pytest.mark.parametrize("variant", ["default", "loader", "strip"])
+@pytest.mark.parametrize("variant", ["default", "loader", "strip", "split"])
 def test_no_stale_shared_memory_reads(ctis, variant):
     """Every projection kernel with CTIS_DEBUG=8 NaN-fills its window ring first: results must not
     change (a band without taps in a forward pass once read a slot it never loaded).  Variants: the
     default kernel choice (odd field stops take the repacked TMA forward), the element-loader forward
-    (CTIS_FWD_REPACK=0) and the strip forward forced on every TMA plan (CTIS_FWD_STRIP=1)."""
+    (CTIS_FWD_REPACK=0), the strip forward forced on every TMA plan (CTIS_FWD_STRIP=1) and the mode-split
+    back projection forced on every plan with the persistent back kernel (CTIS_BACK_SPLIT=4)."""
     import os
     import subprocess
     import sys
@@ -504,6 +505,8 @@ def test_no_stale_shared_memory_reads(ctis, variant):
         env["CTIS_FWD_REPACK"] = "0"
     if variant == "strip":
         env["CTIS_FWD_STRIP"] = "1"
+    if variant == "split":  # mode-split back projection (partial z red.add + update pass) on every plan
+        env["CTIS_BACK_SPLIT"] = "4"
     r = subprocess.run([sys.executable, os.path.join(here, "poison_case.py"), "solvers"], env=env,
                        capture_output=True, text=True, timeout=900)
     print(r.stdout[-2000:])
