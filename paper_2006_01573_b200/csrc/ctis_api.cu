@@ -762,12 +762,12 @@ std::vector<std::pair<int, int>> balanced_chunks(int w, int maxb) {
 int choose_back_nb(const ctis_plan_s& P) {
   if (const char* e = std::getenv("CTIS_BACK_NB")) {  // experiments: 4, 8, 12 or 16
     const int v = std::atoi(e);
-    if (v == 2 || v == 4 || v == 8 || v == 12 || v == 16) return v;
+    if (v == 2 || v == 4 || v == 8 || v == 10 || v == 12 || v == 16) return v;
   }
   if (P.throughput) {  // many frames fill the SMs anyway: minimise chunks x (NB + window cost), NB <= 12
     int best = 12;
     long long bestc = LLONG_MAX;
-    for (int NB : {12, 8, 4, 2}) {
+    for (int NB : {12, 10, 8, 4, 2}) {  // 10: w = 50 (C3/C5) splits into 5 full chunks, no padded band slots
       const long long c = (long long)((P.w + NB - 1) / NB) * (NB + 5);
       if (c < bestc) {
         bestc = c;
@@ -780,7 +780,7 @@ int choose_back_nb(const ctis_plan_s& P) {
   const long long slots = 148LL * 2;
   int best = kBackBandsMax;
   double bestc = 1e300;
-  for (int NB : {16, 12, 8, 4, 2}) {
+  for (int NB : {16, 12, 10, 8, 4, 2}) {
     const long long nch = (P.w + NB - 1) / NB;
     const long long ctas = tiles * nch;
     const double waves = std::ceil((double)ctas / (double)slots);

@@ -1345,11 +1345,13 @@ CTIS_FWD2(2, 8, 40)
 CTIS_BACK4(2, 4, ctis_back4_b2_t)
 CTIS_BACK4(4, 4, ctis_back4_b4_t)
 CTIS_BACK4(8, 4, ctis_back4_b8_t)
+CTIS_BACK4(10, 4, ctis_back4_b10_t)
 CTIS_BACK4(12, 4, ctis_back4_b12_t)
 CTIS_BACK4(16, 4, ctis_back4_b16_t)
 CTIS_BACK4(2, 2, ctis_back2_b2_t)
 CTIS_BACK4(4, 2, ctis_back2_b4_t)
 CTIS_BACK4(8, 2, ctis_back2_b8_t)
+CTIS_BACK4(10, 2, ctis_back2_b10_t)
 CTIS_BACK4(12, 2, ctis_back2_b12_t)
 CTIS_BACK4(16, 2, ctis_back2_b16_t)
 
@@ -1365,6 +1367,7 @@ CTIS_BACK4(16, 2, ctis_back2_b16_t)
 CTIS_BACK(2)
 CTIS_BACK(4)
 CTIS_BACK(8)
+CTIS_BACK(10)
 CTIS_BACK(12)
 CTIS_BACK(16)
 
