@@ -135,9 +135,17 @@ CTIS_API ctis_status ctis_plan_dims(ctis_plan plan, int64_t out[10]);
 
 /* Plan layout (host-side, no device work; tests and profiling): out[0..9] = forward tap pages,
  * back tap pages, forward chunk passes, back chunks, forward uses TMA (0/1), back uses TMA (0/1),
- * back bands per chunk (NB), back tile columns, forward modes per pass (MAXM), forward work items
+ * back bands per chunk (NB), back tile columns, forward kernel (> 0: classic forward with this many
+ * modes per pass; < 0: strip forward with -out[8] consumer warps), forward work items
  * per frame.  A page is one 64 KB __constant__ bank of tap tables (one kernel launch per page and
- * projection).  CTIS_ERR_INVALID_ARGUMENT if plan or out is NULL. */
+ * projection).  CTIS_ERR_INVALID_ARGUMENT if plan or out is NULL.
+ *
+ * Plan-owned scratch, allocated on first use outside any stream capture: a row-repacked copy of f
+ * for field stops with a % 4 != 0 (frames x round4(a) x alpha x w floats; the TMA forward needs a
+ * 16-byte row pitch) and a partial-z buffer (frames x m floats) for plans whose back projection is
+ * mode-split (too few work items to fill the SMs).  ctis_mlem* allocate them before capturing their
+ * CUDA graph; a first forward / back projection captured into the CALLER's graph fails with
+ * CTIS_ERR_CUDA (stream capture) — run one uncaptured call first. */
 CTIS_API ctis_status ctis_plan_info(ctis_plan plan, int64_t out[10]);
 
 CTIS_API ctis_status ctis_set_option(ctis_plan plan, int option, int64_t value);
