@@ -535,7 +535,7 @@ bool strip_desc(const ctis_plan_s& P, const StripPass& ps, int box_r, std::vecto
   all.rmin = (int)std::floor(all.rmin / 4.0) * 4;
   const int tiles_r = (P.a + all.rmax - all.rmin + kFwdTR - 1) / kFwdTR;
   const int tiles_c = (P.alpha + all.cmax - all.cmin + kFwdTC - 1) / kFwdTC;
-  const int BI = kDescHeader + kStripMG * nhg, TP = BI + 4 * nb;
+  const int BI = kDescHeader + 2 * kStripMG * nhg, TP = BI + 4 * nb;
   out.assign(TP + 8 * nb * nhg, 0u);
   out[0] = (uint32_t)ps.b0;
   out[1] = (uint32_t)nb;
@@ -548,6 +548,8 @@ bool strip_desc(const ctis_plan_s& P, const StripPass& ps, int box_r, std::vecto
     for (int k = 0; k < kStripMG; ++k) {
       const Mode* md = k < (int)ps.groups[g].ms.size() ? ps.groups[g].ms[k] : nullptr;
       out[kDescHeader + kStripMG * g + k] = md ? (uint32_t)(md->ref_dr + P.gamma * md->ref_dc) : 0xffffffffu;
+      // the same reference as (row, column) for the TMA flush box (no division in the kernel)
+      out[kDescHeader + kStripMG * (nhg + g) + k] = md ? (uint32_t)md->ref_dr | ((uint32_t)md->ref_dc << 16) : 0u;
     }
   for (int b = 0; b < nb; ++b) {
     // TMA box row origin all.rmin + 32k + row0_rel must be a multiple of 4 (see forward_desc)
@@ -606,6 +608,7 @@ bool build_strip_forward(ctis_plan_s& P, const std::vector<std::pair<int, int>>&
   const char* env = std::getenv("CTIS_FWD_STRIP");
   const int want = env ? std::atoi(env) : -1;  // 0 never, 1 whenever possible, -1 when it pays
   if (want == 0 || !P.tma_f) return false;
+  if (P.gamma >= 65536 || P.xi >= 65536) return false;  // flush references are packed as 16-bit (row, column)
   // Mode references with rows rounded down to a multiple of 4 (o = o_ref + dr + gamma*dc holds for any
   // reference; the shifts grow by <= 3 rows): flush boxes then start on 16-byte FPA row boundaries.
   std::vector<std::vector<Mode>> smodes = chunk_modes;  // outlives every StripGroup pointer below

@@ -74,6 +74,7 @@ constexpr int kBackWinFloats = 3584;    // 14 KB per stage (>= 60 x 56)
 //   [D+0] lam0 [D+1] nb [D+2] nhg (strip groups = consumer warps used) [D+3] u_r0 [D+4] u_c0
 //   [D+5] tiles_r [D+6] tiles_c [D+7] 0
 //   [D+8 ..]          o_ref[g*kStripMG + k] (0xffffffff: empty slot)     (4*nhg words)
+//   [D+8+4*nhg ..]    the same references as ref_row | ref_col << 16     (4*nhg words)
 //   [BI ..]           per band: row0_rel, col0_rel, 0, 0
 //   [TP = BI+4*nb ..] per band b and group g: 8 words at TP + 8*(b*nhg + g):
 //                     [0] strip byte offset into the window (thread base excluded), [1] row offset o_k

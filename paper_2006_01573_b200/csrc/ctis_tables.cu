@@ -1112,7 +1112,7 @@ __device__ __forceinline__ void forward_strip(const TabArgs& A, const CUtensorMa
         const uint32_t D = c_tab[1 + k];
         const int lam0 = tabi(D + 0), nb = tabi(D + 1), nhg = tabi(D + 2), tiles_r = tabi(D + 5);
         const int U_r = tabi(D + 3) + (tile % tiles_r) * kFwdTR, U_c = tabi(D + 4) + (tile / tiles_r) * kFwdTC;
-        const uint32_t BI = D + kDescHeader + MG * nhg;
+        const uint32_t BI = D + kDescHeader + 2 * MG * nhg;
 #pragma unroll 1
         for (int b = 0; b < nb; ++b, ++w) {
           if (w >= S) mbar_wait(empty + 8 * slot, phase ^ 1u);  // consumers released the slot
@@ -1165,7 +1165,7 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
     const int nb = tabi(D + 1), nhg = tabi(D + 2), tiles_r = tabi(D + 5);
     const int U_r = tabi(D + 3) + (tile % tiles_r) * kFwdTR, U_c = tabi(D + 4) + (tile / tiles_r) * kFwdTC;
     const bool act = warp < nhg;
-    const uint4* ent = tab4(D + kDescHeader + MG * nhg + 4 * nb) + 2 * warp;  // band 0, this warp's group
+    const uint4* ent = tab4(D + kDescHeader + 2 * MG * nhg + 4 * nb) + 2 * warp;  // band 0, this warp's group
     const unsigned estep = 2u * nhg;
     float acc[MG][kStripP];
 #pragma unroll
@@ -1245,7 +1245,8 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
     for (int m = 0; m < MG; ++m) {
       const unsigned o = c_tab[D + kDescHeader + MG * warp + m];
       if (o == 0xffffffffu || !((live >> m) & 1u)) continue;
-      const int r0 = U_r + (int)(o % (unsigned)A.gamma), c0 = U_c + (int)(o / (unsigned)A.gamma);
+      const unsigned orc = c_tab[D + kDescHeader + MG * nhg + MG * warp + m];  // o_ref as (row, column)
+      const int r0 = U_r + (int)(orc & 0xffffu), c0 = U_c + (int)(orc >> 16);
       const unsigned tile_s = stage + 2048u * m;
       if (tma_flush && r0 >= 0 && (r0 & 3) == 0 && c0 >= 0 && r0 + kFwdTR <= A.gamma && c0 + kFwdTC <= A.xi) {
         if (lane == 0) tma_reduce_add_3d(tg, tile_s, r0, c0, z);
