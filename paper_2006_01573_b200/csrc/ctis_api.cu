@@ -651,6 +651,12 @@ bool build_strip_forward(ctis_plan_s& P, const std::vector<std::pair<int, int>>&
   box_r = std::max(box_r, 8);
   while (box_r % 8 != 4) ++box_r;  // pitch / 4 odd: conflict-free float4 strip loads across columns
   if (box_r > 256 || box_c > 256 || (long long)box_r * box_c > kTmaWinFloats) return false;
+  {  // shared memory: barriers + >= 3 window slots + 1 KB alignment slack + staging of the widest pass
+    size_t wm = 0;
+    for (const StripPass& ps : passes) wm = std::max(wm, ps.groups.size());
+    const size_t slot_b = (size_t)((box_r * box_c + 31) / 32 * 32) * sizeof(float);
+    if (128 + 3 * slot_b + 2048 + wm * kStripStage * sizeof(float) > 227 * 1024) return false;
+  }
   std::vector<std::vector<uint32_t>> descs;
   std::vector<int> tiles, warps;
   for (const StripPass& ps : passes) {
