@@ -58,7 +58,10 @@ constexpr int kModeSpanMax = 32;
 constexpr int kFwdBandsTma = 25;
 constexpr int kModeSpanTma = 16;
 constexpr int kFwdStages = 8;           // window pipeline depth (TMA boxes / cp.async groups in flight),
-constexpr int kBackStages = 8;          // refilled K = stages/2 at a time
+#ifndef CTIS_BACK_STAGES
+#define CTIS_BACK_STAGES 8
+#endif
+constexpr int kBackStages = CTIS_BACK_STAGES;  // back ring depth (refilled every CTIS_BACK_K windows)
 constexpr int kFwdWinFloats = 2560;     // element-loader slot: 10 KB per stage (>= 56 x 40)
 constexpr int kTmaWinFloats = 8192;     // TMA box cap (32 KB)
 constexpr int kBackWinFloats = 3584;    // 14 KB per stage (>= 60 x 56)
