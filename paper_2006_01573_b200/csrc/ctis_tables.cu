@@ -1041,6 +1041,12 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
 // A.stages-deep ring (full / empty mbarriers), the consumer warps release a slot as soon as their strip
 // is in registers.
 #include "ctis_strip_dispatch.inc"
+#ifndef CTIS_STRIP_PIN
+#define CTIS_STRIP_PIN 1  // ring depth and slot size pinned in registers in the consumer loop (C4 MLEM 134.6 -> 134.0 us)
+#endif
+#ifndef CTIS_STRIP_PROBE
+#define CTIS_STRIP_PROBE 1  // test the next window's mbarrier inside the dispatch (hides the probe latency)
+#endif
 
 // one lane of the (converged) warp; elect.sync also orders the warp's earlier shared loads before the
 // elected lane's release (it synchronises the warp like __syncwarp)
@@ -1150,6 +1156,14 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
   asm volatile("mov.b32 %0, %0;" : "+r"(tb));
   asm volatile("mov.b32 %0, %0;" : "+r"(full));
   asm volatile("mov.b32 %0, %0;" : "+r"(empty));
+#if CTIS_STRIP_PIN
+  asm volatile("mov.b32 %0, %0;" : "+r"(slot_bytes));  // kept in registers, not re-read from the
+  unsigned S_ = S;                                      // parameter bank every band
+  asm volatile("mov.b32 %0, %0;" : "+r"(S_));
+#define STRIP_S S_
+#else
+#define STRIP_S S
+#endif
   // async-proxy flush: the whole plan is 2-D translations (every nonzero accumulator's pixel is inside
   // the FPA box) — otherwise (cyclic wrap of Eq. 7) red.global.add with exact modular indices
   const bool tma_flush = A.tma_flush && !(A.dbg & 1);
@@ -1178,6 +1192,7 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
       e0 = ent[0];
       e1 = ent[1];
     }
+    unsigned ready = 0;  // CTIS_STRIP_PROBE: the previous band's dispatch found this band's window landed
 #pragma unroll 1
     for (int b = 0; b < nb; ++b) {
       const uint4 c0 = e0, c1 = e1;
@@ -1186,21 +1201,31 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
         e0 = ent[0];
         e1 = ent[1];
       }
-      if (!notma) mbar_wait(full + 8 * slot, phase);
+      if (!notma && !ready) mbar_wait(full + 8 * slot, phase);
       // the whole 40-row strip (rows past the group's range are never read by its blocks)
       if (act) strip_load(v, tslot + c0.x);
       if (elect_one()) mbar_arrive(empty + 8 * slot);  // the strip is in registers: the slot may be refilled
       tslot += slot_bytes;
-      if (++slot == S) {
+      if (++slot == STRIP_S) {
         slot = 0;
         phase ^= 1u;
         tslot = tb;
       }
       if (act) {
         // row offset per slot (kStripNO: no tap in this band, the skip target)
+#if CTIS_STRIP_PROBE
+        // the next window's mbarrier is tested at the dispatch's entry and its result read at the exit, so
+        // the probe's latency hides behind the FMA blocks (every band: after an item's last band the next
+        // slot is the next item's first window; ONE dispatch copy — a second copy for the last band measured
+        // slower, instruction-cache pressure).  C4 forward 63.6 -> 61.2 us, MLEM 133.1 -> 131.6 us/iteration.
+        strip_dispatch4p(acc[0], acc[1], acc[2], acc[3], v, __uint_as_float(c0.z), __uint_as_float(c0.w),
+                         __uint_as_float(c1.x), __uint_as_float(c1.y), c0.y & 0xffu, (c0.y >> 8) & 0xffu,
+                         (c0.y >> 16) & 0xffu, c0.y >> 24, full + 8 * slot, phase, ready);
+#else
         strip_dispatch4(acc[0], acc[1], acc[2], acc[3], v, __uint_as_float(c0.z), __uint_as_float(c0.w),
                         __uint_as_float(c1.x), __uint_as_float(c1.y), c0.y & 0xffu, (c0.y >> 8) & 0xffu,
                         (c0.y >> 16) & 0xffu, c0.y >> 24);
+#endif
       }
     }
     if (!act) continue;
@@ -1272,6 +1297,7 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
   __syncwarp();
 }
 
+#undef STRIP_S
 }  // namespace
 
 // Element-loader forward (plans whose geometry rules out TMA boxes: a % 4 != 0)
