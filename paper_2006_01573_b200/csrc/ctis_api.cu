@@ -1466,7 +1466,11 @@ cudaError_t launch_pages(ctis_plan_s& P, const std::vector<Page>& pages, const f
     // TMA kernels are persistent (2 CTAs per SM walk the page's items); element-loader kernels are
     // one CTA per (tile, chunk, frame)
     const long long items = (long long)pg.total_items * frames;
-    const int per_sm = 2;  // resident CTAs per SM (persistent TMA kernels)
+    int per_sm = 2;  // resident CTAs per SM (persistent TMA kernels)
+    if (!fwd && tma) {  // experiment switch: more resident back CTAs (kernels built with CTIS_BACK2_MINB)
+      static const int env_per_sm = std::getenv("CTIS_BACK_PER_SM") ? std::atoi(std::getenv("CTIS_BACK_PER_SM")) : 0;
+      if (env_per_sm > 0) per_sm = env_per_sm;
+    }
     dim3 grid = tma ? dim3((unsigned)std::min<long long>(items, (long long)per_sm * P.sms), 1, 1)
                     : dim3(pg.max_tiles, pg.nchunks, frames);
     bool coop = false;

@@ -976,7 +976,10 @@ __device__ __forceinline__ void back_persistent4(const TabArgs& A, const CUtenso
     // band's loads above the previous band's stores to the same array)
     float* f = A.dst + (long long)z * A.dst_frame;
     const int qr = q_r0 + lane;
-    constexpr int EG = NB < 6 ? NB : 6;
+#ifndef CTIS_BACK_EG
+#define CTIS_BACK_EG 6  // epilogue: bands whose f loads are issued together
+#endif
+    constexpr int EG = NB < CTIS_BACK_EG ? NB : CTIS_BACK_EG;
     if (A.mode == 3) {  // mode-split plans: add this mode subset's partial z (ctis_api.cu enqueue_back)
       if (qr < A.a) {
 #pragma unroll
@@ -1361,8 +1364,14 @@ CTIS_FWD2(2, 8, 32)
 CTIS_FWD2(2, 8, 36)
 CTIS_FWD2(2, 8, 40)
 
+#ifndef CTIS_BACK2_MINB
+#define CTIS_BACK2_MINB 2  // resident CTAs per SM the 32 x 16-tile back kernels are compiled for
+#endif
+#ifndef CTIS_BACK4_MINB
+#define CTIS_BACK4_MINB 2  // resident CTAs per SM the 32 x 32-tile back kernels are compiled for
+#endif
 #define CTIS_BACK4(NB, POS, NAME)                                                                          \
-  extern "C" __global__ void __launch_bounds__(kBack4Threads, 2)                                           \
+  extern "C" __global__ void __launch_bounds__(kBack4Threads, POS == 2 ? CTIS_BACK2_MINB : CTIS_BACK4_MINB) \
       NAME(const TabArgs A, const __grid_constant__ CUtensorMap tm) {                                      \
     if (A.frames == 0) return;                                                                             \
     pdl_enter();                                                                                           \
