@@ -26,7 +26,7 @@ if [ "${NCU:-1}" = "1" ]; then
     ncu -i gpurun_out/${TAG}_prof_$k.ncu-rep --page source --csv --print-source sass > gpurun_out/${TAG}_src_$k.csv 2>&1
   done
 fi
-if [ "${SAN:-1}" = "1" ]; then
+if [ "${SAN:-0}" = "1" ]; then
   timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python tools/san_case.py bench > gpurun_out/${TAG}_san_memcheck_bench.txt 2>&1; echo "exit $?" >> gpurun_out/${TAG}_san_memcheck_bench.txt
   CTIS_FWD_STRIP=1 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python tools/san_case.py bench > gpurun_out/${TAG}_san_memcheck_strip.txt 2>&1; echo "exit $?" >> gpurun_out/${TAG}_san_memcheck_strip.txt
   timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python tools/san_case.py loader > gpurun_out/${TAG}_san_memcheck_loader.txt 2>&1; echo "exit $?" >> gpurun_out/${TAG}_san_memcheck_loader.txt
