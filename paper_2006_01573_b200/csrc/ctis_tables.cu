@@ -1079,8 +1079,7 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 template <int MG>
 __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CUtensorMap* tg, int warp, int lane,
                                                       int per_frame, int nch, int items, unsigned sbase,
-                                                      unsigned slot_bytes, unsigned full, unsigned empty,
-                                                      unsigned stage);
+                                                      unsigned slot_bytes, unsigned full, unsigned stage);
 
 template <int MG>
 __device__ __forceinline__ void forward_strip(const TabArgs& A, const CUtensorMap* tm, const CUtensorMap* tg) {
@@ -1136,7 +1135,7 @@ __device__ __forceinline__ void forward_strip(const TabArgs& A, const CUtensorMa
       }
     }
   } else {
-    forward_strip_consume<MG>(A, tg, warp, lane, per_frame, nch, items, sbase, slot_bytes, full, empty,
+    forward_strip_consume<MG>(A, tg, warp, lane, per_frame, nch, items, sbase, slot_bytes, full,
                               stage0 + 4u * kStripStage * warp);
   }
   if (A.ratio_mode) {  // fused ratio (CTIS_OPT_FUSED_RATIO): one CTA per SM, cooperative launch
@@ -1148,8 +1147,7 @@ __device__ __forceinline__ void forward_strip(const TabArgs& A, const CUtensorMa
 template <int MG>
 __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CUtensorMap* tg, int warp, int lane,
                                                       int per_frame, int nch, int items, unsigned sbase,
-                                                      unsigned slot_bytes, unsigned full, unsigned empty,
-                                                      unsigned stage) {
+                                                      unsigned slot_bytes, unsigned full, unsigned stage) {
   const unsigned S = (unsigned)A.stages;
   constexpr int NV = 4 * kStripNQ;
   // ---- consumers: lane = rs + 2*col owns rows 16*rs .. 16*rs+15 of u column col of the 32 x 16 tile
@@ -1158,7 +1156,6 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
   // opaque copies: ptxas would otherwise re-derive these addresses (S2R, LDC) in every band iteration
   asm volatile("mov.b32 %0, %0;" : "+r"(tb));
   asm volatile("mov.b32 %0, %0;" : "+r"(full));
-  asm volatile("mov.b32 %0, %0;" : "+r"(empty));
 #if CTIS_STRIP_PIN
   asm volatile("mov.b32 %0, %0;" : "+r"(slot_bytes));  // kept in registers, not re-read from the
   unsigned S_ = S;                                      // parameter bank every band
@@ -1171,7 +1168,12 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
   // the FPA box) — otherwise (cyclic wrap of Eq. 7) red.global.add with exact modular indices
   const bool tma_flush = A.tma_flush && !(A.dbg & 1);
   float v[NV];
-  unsigned slot = 0, phase = 0, tslot = tb;  // tslot: this thread's strip base in the current slot
+  unsigned phase = 0, tslot = tb;  // tslot: this thread's strip base in the current slot
+  // ring position as the full-barrier address (the empty barrier of a slot sits 8 * kStripStagesMax bytes
+  // above its full barrier): one add and compare per band, and the release reads an address register
+  // that is not rewritten before the next band (C4 forward 60.7 -> 60.0 us, with the 32-bit entry index)
+  unsigned fslot = full;
+  const unsigned fend = full + 8u * STRIP_S;
   unsigned notma = A.dbg & 1;  // profiling switch, pinned in a register (not re-read every band)
   asm volatile("mov.b32 %0, %0;" : "+r"(notma));
   bool staged = false;  // bulk reductions of this warp's staging tiles may still be reading them
@@ -1182,8 +1184,10 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
     const int nb = tabi(D + 1), nhg = tabi(D + 2), tiles_r = tabi(D + 5);
     const int U_r = tabi(D + 3) + (tile % tiles_r) * kFwdTR, U_c = tabi(D + 4) + (tile / tiles_r) * kFwdTC;
     const bool act = warp < nhg;
-    const uint4* ent = tab4(D + kDescHeader + 2 * MG * nhg + 4 * nb) + 2 * warp;  // band 0, this warp's group
-    const unsigned estep = 2u * nhg;
+    // entry index in uint4 units (32-bit: no 64-bit pointer arithmetic per band)
+    uint32_t ei = (D + kDescHeader + 2 * MG * nhg + 4 * nb) / 4 + 2 * warp;
+    const uint32_t estep = 2u * nhg;
+    const uint4* c4 = reinterpret_cast<const uint4*>(c_tab);
     float acc[MG][kStripP];
 #pragma unroll
     for (int m = 0; m < MG; ++m)
@@ -1192,25 +1196,26 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
     // tap entries are software-pipelined one band ahead (constant-cache latency overlaps a band's FMAs)
     uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = e0;
     if (act) {
-      e0 = ent[0];
-      e1 = ent[1];
+      e0 = c4[ei];
+      e1 = c4[ei + 1];
     }
     unsigned ready = 0;  // CTIS_STRIP_PROBE: the previous band's dispatch found this band's window landed
 #pragma unroll 1
     for (int b = 0; b < nb; ++b) {
       const uint4 c0 = e0, c1 = e1;
       if (act && b + 1 < nb) {
-        ent += estep;
-        e0 = ent[0];
-        e1 = ent[1];
+        ei += estep;
+        e0 = c4[ei];
+        e1 = c4[ei + 1];
       }
-      if (!notma && !ready) mbar_wait(full + 8 * slot, phase);
-      // the whole 40-row strip (rows past the group's range are never read by its blocks)
+      const unsigned fcur = fslot;
+      if (!notma && !ready) mbar_wait(fcur, phase);
       if (act) strip_load(v, tslot + c0.x);
-      if (elect_one()) mbar_arrive(empty + 8 * slot);  // the strip is in registers: the slot may be refilled
+      if (elect_one()) mbar_arrive(fcur + 8u * kStripStagesMax);
       tslot += slot_bytes;
-      if (++slot == STRIP_S) {
-        slot = 0;
+      fslot += 8u;
+      if (fslot == fend) {
+        fslot = full;
         phase ^= 1u;
         tslot = tb;
       }
@@ -1223,7 +1228,7 @@ __device__ __forceinline__ void forward_strip_consume(const TabArgs& A, const CU
         // slower, instruction-cache pressure).  C4 forward 63.6 -> 61.2 us, MLEM 133.1 -> 131.6 us/iteration.
         strip_dispatch4p(acc[0], acc[1], acc[2], acc[3], v, __uint_as_float(c0.z), __uint_as_float(c0.w),
                          __uint_as_float(c1.x), __uint_as_float(c1.y), c0.y & 0xffu, (c0.y >> 8) & 0xffu,
-                         (c0.y >> 16) & 0xffu, c0.y >> 24, full + 8 * slot, phase, ready);
+                         (c0.y >> 16) & 0xffu, c0.y >> 24, fslot, phase, ready);
 #else
         strip_dispatch4(acc[0], acc[1], acc[2], acc[3], v, __uint_as_float(c0.z), __uint_as_float(c0.w),
                         __uint_as_float(c1.x), __uint_as_float(c1.y), c0.y & 0xffu, (c0.y >> 8) & 0xffu,
