@@ -40,7 +40,35 @@ __global__ void ratio_kernel(const float* __restrict__ g, float* gh, float* r,
                          reinterpret_cast<uintptr_t>(r)) & 15u) == 0;
   const long long n4 = aligned ? (count >> 2) : 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+#ifndef CTIS_RATIO_UNROLL
+#define CTIS_RATIO_UNROLL 1  // measured (B200, C4, with 4 blocks per SM): 128.2 -> 127.7 us per iteration
+#endif
+#if CTIS_RATIO_UNROLL
+  // two float4 per thread and iteration: the loads of both issued before any division
+  for (; t0 + stride < n4; t0 += 2 * stride) {
+    const long long i0 = t0, i1 = t0 + stride;
+    const float4 gv0 = __ldg(reinterpret_cast<const float4*>(g) + i0);
+    const float4 gv1 = __ldg(reinterpret_cast<const float4*>(g) + i1);
+    const float4 hv0 = reinterpret_cast<const float4*>(gh)[i0];
+    const float4 hv1 = reinterpret_cast<const float4*>(gh)[i1];
+    float4 o0, o1;
+    o0.x = hv0.x > 0.f ? __fdiv_rn(gv0.x, hv0.x) : 0.f;
+    o0.y = hv0.y > 0.f ? __fdiv_rn(gv0.y, hv0.y) : 0.f;
+    o0.z = hv0.z > 0.f ? __fdiv_rn(gv0.z, hv0.z) : 0.f;
+    o0.w = hv0.w > 0.f ? __fdiv_rn(gv0.w, hv0.w) : 0.f;
+    o1.x = hv1.x > 0.f ? __fdiv_rn(gv1.x, hv1.x) : 0.f;
+    o1.y = hv1.y > 0.f ? __fdiv_rn(gv1.y, hv1.y) : 0.f;
+    o1.z = hv1.z > 0.f ? __fdiv_rn(gv1.z, hv1.z) : 0.f;
+    o1.w = hv1.w > 0.f ? __fdiv_rn(gv1.w, hv1.w) : 0.f;
+    reinterpret_cast<float4*>(r)[i0] = o0;
+    reinterpret_cast<float4*>(r)[i1] = o1;
+    if (zero_ghat) {
+      reinterpret_cast<float4*>(gh)[i0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      reinterpret_cast<float4*>(gh)[i1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+#endif
   for (long long i = t0; i < n4; i += stride) {
     const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + i);
     const float4 hv = reinterpret_cast<const float4*>(gh)[i];
@@ -61,8 +89,11 @@ __global__ void ratio_kernel(const float* __restrict__ g, float* gh, float* r,
 
 cudaError_t launch_ratio(const float* g, float* ghat, float* r, long long count, bool zero_ghat, cudaStream_t s,
                          bool pdl) {
+#ifndef CTIS_RATIO_BPS
+#define CTIS_RATIO_BPS 4  // blocks of 256 threads per SM (8 / 16 without the unroll: 128.2 / 128.0 us)
+#endif
   const long long want = (count / 4 + 255) / 256;
-  const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
+  const int blocks = (int)(want < 148 * CTIS_RATIO_BPS ? (want > 0 ? want : 1) : 148 * CTIS_RATIO_BPS);
   return launch_ex(ratio_kernel, blocks, 256, s, pdl, g, ghat, r, count, zero_ghat ? 1 : 0);
 }
 
