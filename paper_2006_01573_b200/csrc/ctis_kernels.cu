@@ -143,19 +143,19 @@ cudaError_t launch_ratio_box(const float* g, float* ghat, float* r, long long n,
 
 // Row repack of f for the TMA forward (plans with a % 4 != 0): one thread per element.
 __global__ void repack_rows_kernel(const float* __restrict__ src, float* __restrict__ dst, int a, int pitch,
-                                   long long total) {
+                                   long long cols) {
   pdl_enter();
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long c = i / a;
-    dst[c * pitch + (i - c * a)] = __ldg(src + i);
-  }
+  // one warp per column (lanes stride over its a rows): no integer division per element
+  const int lane = threadIdx.x & 31;
+  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long c = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); c < cols; c += wstride)
+    for (int r = lane; r < a; r += 32) dst[c * pitch + r] = __ldg(src + c * a + r);
 }
 
 cudaError_t launch_repack_rows(const float* src, float* dst, int a, int pitch, long long cols, cudaStream_t s) {
-  const long long total = (long long)a * cols;
-  const long long want = (total + 255) / 256;
+  const long long want = (cols + 7) / 8;  // 8 warps (columns) per block
   const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
-  return launch_ex(repack_rows_kernel, blocks, 256, s, false, src, dst, a, pitch, total);
+  return launch_ex(repack_rows_kernel, blocks, 256, s, false, src, dst, a, pitch, cols);
 }
 
 // Update pass of mode-split back projections (ctis_api.cu enqueue_back): the epilogue's arithmetic
@@ -163,9 +163,12 @@ cudaError_t launch_repack_rows(const float* src, float* dst, int a, int pitch, l
 __global__ void split_update_kernel(float* f, float* z, const float* __restrict__ invh, int ell, int w,
                                     long long count, int mode) {
   pdl_enter();
-  const long long m = (long long)ell * w;
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < count; j += (long long)gridDim.x * blockDim.x) {
-    const float ih = __ldg(invh + (j % m) / ell);
+  // blockIdx.y = frame, blockIdx.x strides over the frame's m = ell * w voxels with 32-bit band index math
+  const unsigned m = (unsigned)ell * (unsigned)w;
+  const long long base = (long long)blockIdx.y * m;
+  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
+    const long long j = base + k;
+    const float ih = __ldg(invh + k / (unsigned)ell);
     const float zz = z[j];
     z[j] = 0.f;
     f[j] = mode == 1 ? f[j] * zz * ih : mode == 2 ? f[j] * expf(zz * ih) : zz;
@@ -174,9 +177,21 @@ __global__ void split_update_kernel(float* f, float* z, const float* __restrict_
 
 cudaError_t launch_split_update(float* f, float* z, const float* invh, int ell, int w, long long count, int mode,
                                 cudaStream_t s) {
-  const long long want = (count + 255) / 256;
-  const int blocks = (int)(want < 148 * 8 ? (want > 0 ? want : 1) : 148 * 8);
-  return launch_ex(split_update_kernel, blocks, 256, s, false, f, z, invh, ell, w, count, mode);
+  const long long m = (long long)ell * w;
+  const long long frames = m > 0 ? count / m : 0;
+  if (frames < 1) return cudaSuccess;
+  const long long want = (m + 255) / 256;
+  const long long cap = std::max<long long>(1, 148LL * 8 / frames);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)std::max<long long>(1, std::min(want, cap)), (unsigned)frames);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, split_update_kernel, f, z, invh, ell, w, count, mode);
 }
 
 __global__ void sensitivity_kernel(const float* __restrict__ hband, float* __restrict__ h, int ell, int m) {
